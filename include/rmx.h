@@ -1,0 +1,175 @@
+/*
+ * rmx.h - C ABI of librmx, the B200-native (sm_100a) outer-region energy sweep of the
+ * R-matrix method (McLaughlin & Ballance, arxiv 1403.5524):
+ *
+ *     R(E)  = (1/2a) W diag(1/(E_k - E)) W^T                      (§6 Eq. 1-2,
+ *                                                                  north_star convention, BASELINE.json:5)
+ *     K(E)  = -(G - aR G')^{-1} (F - aR F')                       (BASELINE.json:5)
+ *     T(E)  = 2i K_oo (I - i K_oo)^{-1},  |T_ij|^2                (BASELINE.json:5)
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - All floating-point arrays are IEEE fp64, row-major, C-contiguous unless a leading
+ *    dimension is given. "DEVICE" pointers are CUDA device memory of the ctx's device;
+ *    "HOST" pointers are ordinary (preferably pinned) host memory.
+ *  - Ownership: the caller owns every buffer it passes; the library owns only the
+ *    workspace inside rmx_ctx. No buffer is retained after a call returns.
+ *  - Asynchrony: device-pointer calls are enqueued on the ctx's CUDA stream and return
+ *    before the kernels finish; results are valid after the stream is synchronised
+ *    (rmx_sync, cudaStreamSynchronize, or a later operation on the same stream).
+ *    The only host allocation/cudaMalloc happens when the workspace must grow (first call
+ *    at a larger shape); the hot loop of rmx_sweep allocates nothing.
+ *  - Call-level errors (rmx_rc) are synchronous argument checks: a null pointer, a
+ *    non-positive size, a <= 0, a bad leading dimension or alignment. (n_open lives on the
+ *    device and cannot be checked synchronously: kernels clamp it to [0, nch].) On an
+ *    error nothing is enqueued and
+ *    rmx_last_error() describes it. RMX_ECUDA reports a CUDA launch/runtime error
+ *    (sticky errors are also returned by the next call or by rmx_sync).
+ *  - Per-energy problems never abort a batch. They are reported in the caller's int32
+ *    status[ne] array, which the caller must initialise (e.g. to 0 = RMX_E_OK) before
+ *    the first call of a pipeline. A call writes a code only into entries that are still
+ *    RMX_E_OK (first error wins), so one status array can follow an energy through
+ *    build_R -> match_K -> collision_strength. Outputs of a flagged energy are NaN (POLE)
+ *    or undefined-but-finite-or-NaN (SINGULAR / NONFINITE).
+ *  - Preconditions (not checked, documented; rmx_synth guarantees them): E_k ascending;
+ *    channels sorted by threshold so the open set is the prefix [0, n_open); closed-
+ *    channel entries of F,G,F',G' satisfy F=G, F'=G' (the e^{-kappa a} functions of
+ *    BASELINE.json:9, reading M3), so the closed columns of K are exactly -e_j.
+ */
+#ifndef RMX_H
+#define RMX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rmx_ctx rmx_ctx;
+
+typedef enum {
+  RMX_OK = 0,      /* success                                   */
+  RMX_EINVAL = 1,  /* bad argument (synchronous; nothing launched) */
+  RMX_ENOMEM = 2,  /* workspace / pinned staging allocation failed */
+  RMX_ECUDA = 3    /* CUDA runtime / launch error                */
+} rmx_rc;
+
+/* per-energy status codes written into int32 status[ne] */
+enum {
+  RMX_E_OK = 0,
+  RMX_E_POLE = 1,      /* |E - E_k| < 1e-10 Ry for some k; outputs NaN */
+  RMX_E_SINGULAR = 2,  /* exact zero pivot in the matching LU (LAPACK info > 0 style) */
+  RMX_E_NONFINITE = 3  /* a non-finite value reached K or |T|^2 */
+};
+
+/* Create a context on CUDA device `device`, enqueuing on `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream). */
+rmx_rc rmx_create(rmx_ctx **ctx, int device, void *cuda_stream);
+rmx_rc rmx_destroy(rmx_ctx *ctx);
+/* Change the stream subsequent calls enqueue on (e.g. torch's current stream). */
+rmx_rc rmx_set_stream(rmx_ctx *ctx, void *cuda_stream);
+/* Human-readable description of the last call-level error of this ctx ("" if none). */
+const char *rmx_last_error(const rmx_ctx *ctx);
+
+/*
+ * rmx_build_R - S1+S2: R_ij(E_e) = (1/2a) sum_k w_ik w_jk / (E_k - E_e)   (Eq.1-2;
+ * BASELINE.json:5). Upper triangle computed by an energy-batched FP64 DMMA contraction with
+ * TMA-staged W tiles; the denominators 1/(E_k - E) are formed on chip, never stored. R is
+ * written full and BITWISE symmetric (upper triangle mirrored).
+ *   w      DEVICE [nch][ldw]  amplitudes, k contiguous; ldw >= nlev, ldw even (ldw*8 % 16 == 0,
+ *                             TMA stride rule) and w 16-byte aligned
+ *   Ek     DEVICE [nlev]      poles, ascending
+ *   E      DEVICE [ne]        energies
+ *   R      DEVICE [ne][nch][nch]  output
+ *   status DEVICE int32 [ne]  RMX_E_POLE where min_k |E - E_k| < 1e-10 (R is NaN there)
+ * Errors: EINVAL on null pointers, nch/nlev/ne < 1, a <= 0 or a bad ldw/alignment.
+ */
+rmx_rc rmx_build_R(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                   int64_t nlev, double a, const double *E, int64_t ne, double *R,
+                   int32_t *status);
+
+/*
+ * rmx_match_K - S3+S4: K = -(G - aRG')^{-1}(F - aRF') per energy (BASELINE.json:5), with
+ * A_ij = G_i d_ij - a R_ij G'_j, B_ij = F_i d_ij - a R_ij F'_j. One CTA per energy runs a
+ * blocked right-looking LU with partial pivoting of A (FP64 DMMA trailing updates) on the
+ * augmented matrix [A | B_open]; the n_open open columns are solved, the closed columns
+ * are written as -e_j (precondition above).
+ *   R              DEVICE [ne][nch][nch]
+ *   F, G, Fp, Gp   DEVICE [ne][nch] asymptotic functions at r = a
+ *   n_open         DEVICE int32 [ne] or NULL (= all nch open)
+ *   K              DEVICE [ne][nch][nch] output
+ *   status         DEVICE int32 [ne]: RMX_E_SINGULAR on an exact zero pivot,
+ *                  RMX_E_NONFINITE if K_oo is not finite
+ */
+rmx_rc rmx_match_K(rmx_ctx *ctx, const double *R, const double *F, const double *G,
+                   const double *Fp, const double *Gp, double a, int64_t nch, int64_t ne,
+                   const int32_t *n_open, double *K, int32_t *status);
+
+/*
+ * rmx_collision_strength - S5: T = 2i K_oo (I - i K_oo)^{-1}, o = n_open, via the real
+ * SPD route (BASELINE.json:5; reading T2): S = I + K_oo K_oo^T, Cholesky S = LL^T,
+ * X = S^{-1} K_oo, P = K_oo X; then Re T = -2P, Im T = 2X and |T_ij|^2 = 4(X_ij^2 + P_ij^2).
+ *   K       DEVICE [ne][nch][nch] (only the open block is read)
+ *   T2      DEVICE [ne][nch][nch] or NULL: |T|^2, open block top-left, 0 elsewhere
+ *   rowsum  DEVICE [ne][nch] or NULL: sum_j |T_ij|^2 (0 for closed rows)
+ *   status  DEVICE int32 [ne]: RMX_E_NONFINITE if a non-finite |T|^2 value arises
+ */
+rmx_rc rmx_collision_strength(rmx_ctx *ctx, const double *K, int64_t nch, int64_t ne,
+                              const int32_t *n_open, double *T2, double *rowsum,
+                              int32_t *status);
+
+/*
+ * rmx_sweep - the fused streaming driver: for energies in batches of `batch`, runs
+ * build_R -> match_K -> collision_strength on ctx workspace (R and K never leave the
+ * device), writing only the per-energy summaries rowsum [ne][nch] and status [ne].
+ * Per-energy arithmetic does not depend on the batch position or `batch`, so results are
+ * bitwise identical for any batching / sharding.
+ *   All array arguments DEVICE, shapes as above; F,G,Fp,Gp,n_open are per energy [ne].
+ *   dump_idx  HOST int64 [n_dump] or NULL: energy indices (into [0, ne)) whose full R, K and
+ *             |T|^2 are also written to R_d, K_d, T2_d (each DEVICE [n_dump][nch][nch] or NULL),
+ *             in dump_idx order (the parity sample)
+ *   batch <= 0 selects the default (a multiple of the SM count).
+ */
+rmx_rc rmx_sweep(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                 int64_t nlev, double a, const double *E, int64_t ne, const double *F,
+                 const double *G, const double *Fp, const double *Gp, const int32_t *n_open,
+                 int64_t batch, const int64_t *dump_idx, int64_t n_dump, double *R_d,
+                 double *K_d, double *T2_d, double *rowsum, int32_t *status);
+
+/*
+ * rmx_sweep_host - rmx_sweep with HOST inputs and outputs: copies w (as [nch][ldw]), Ek,
+ * E, F, G, Fp, Gp, n_open host->device (staged through ctx pinned buffers), runs the sweep
+ * and copies rowsum and status back, then synchronises the stream. status is fully
+ * overwritten (initialised to RMX_E_OK internally). Used for the end-to-end measurement.
+ * h2d_bytes / d2h_bytes (may be NULL) receive the bytes moved by this call.
+ */
+rmx_rc rmx_sweep_host(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek,
+                      int64_t nch, int64_t nlev, double a, const double *E, int64_t ne,
+                      const double *F, const double *G, const double *Fp, const double *Gp,
+                      const int32_t *n_open, int64_t batch, double *rowsum, int32_t *status,
+                      int64_t *h2d_bytes, int64_t *d2h_bytes);
+
+/* Synchronise ctx's stream; if n_bad_status/status given, counts nonzero entries of the
+ * DEVICE int32 status[ne] (pass status=NULL to skip). Returns sticky CUDA errors. */
+rmx_rc rmx_sync(rmx_ctx *ctx, const int32_t *status, int64_t ne, int64_t *n_bad);
+
+/* ---- instrumentation (bench / roofline evidence; not needed for correctness) ----------
+ * When enabled, every kernel launch is bracketed by cudaEvents on the ctx stream and its
+ * duration accumulated per kernel id: 0 = R formation, 1 = matching, 2 = T epilogue,
+ * 3 = other (pole scan, packing). rmx_stats reads (total ms, launch count) per id and the
+ * total number of kernel launches since the last reset (counted whether or not timing is
+ * enabled). */
+enum { RMX_KID_RFORM = 0, RMX_KID_MATCH = 1, RMX_KID_TEPI = 2, RMX_KID_OTHER = 3, RMX_NKID = 4 };
+rmx_rc rmx_set_timing(rmx_ctx *ctx, int enable);
+rmx_rc rmx_reset_stats(rmx_ctx *ctx);
+rmx_rc rmx_stats(rmx_ctx *ctx, double *ms_per_kid /* [RMX_NKID] */,
+                 int64_t *launches_per_kid /* [RMX_NKID] */, int64_t *total_launches);
+
+/* Library version (major*10000 + minor*100 + patch) and the compiled SM target (100). */
+int rmx_version(void);
+int rmx_sm_target(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RMX_H */

@@ -1,0 +1,317 @@
+"""paper_1403_5524_b200 - B200-native outer-region R-matrix energy sweep (arxiv 1403.5524).
+
+Thin Python binding over the C-ABI library ``librmx.so`` (declared in ``include/rmx.h``):
+argument marshalling only. Every step of R(E) -> K(E) -> |T(E)|^2 runs in the sm_100a CUDA
+kernels of ``csrc/``; PyTorch supplies device memory, the current CUDA stream and (in
+``paper_1403_5524_b200.dist``) process groups. There is no CPU or PyTorch fallback: if the
+library is missing or no CUDA device is present the calls raise.
+
+    import paper_1403_5524_b200 as rmx
+    ctx = rmx.Context()                       # on torch.cuda.current_device()
+    R, st = ctx.build_R(w, Ek, a, E)          # rmx_build_R
+    K, st = ctx.match_K(R, F, G, Fp, Gp, a, n_open, status=st)       # rmx_match_K
+    T2, rs, st = ctx.collision_strength(K, n_open, status=st)         # rmx_collision_strength
+    out = ctx.sweep(w, Ek, a, E, F, G, Fp, Gp, n_open)                # rmx_sweep (fused driver)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librmx.so")
+
+RMX_OK, RMX_EINVAL, RMX_ENOMEM, RMX_ECUDA = 0, 1, 2, 3
+E_OK, E_POLE, E_SINGULAR, E_NONFINITE = 0, 1, 2, 3
+KID_RFORM, KID_MATCH, KID_TEPI, KID_OTHER = 0, 1, 2, 3
+KID_NAMES = ("rform", "match", "tepi", "other")
+
+# every symbol include/rmx.h declares (tests/test_abi.py checks the header and the .so agree)
+EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rmx_build_R",
+            "rmx_match_K", "rmx_collision_strength", "rmx_sweep", "rmx_sweep_host", "rmx_sync",
+            "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version", "rmx_sm_target")
+
+
+class RmxError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """dlopen librmx.so and declare the C signatures (no CUDA call is made here)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"librmx.so not built at {path}: run `python -m paper_1403_5524_b200.build`"
+                          " (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    P, i64, d, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    sig = {
+        "rmx_create": [ctypes.POINTER(P), i32, P],
+        "rmx_destroy": [P],
+        "rmx_set_stream": [P, P],
+        "rmx_build_R": [P, P, i64, P, i64, i64, d, P, i64, P, P],
+        "rmx_match_K": [P, P, P, P, P, P, d, i64, i64, P, P, P],
+        "rmx_collision_strength": [P, P, i64, i64, P, P, P, P],
+        "rmx_sweep": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, i64, P, P, P, P, P],
+        "rmx_sweep_host": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, P, P, P],
+        "rmx_sync": [P, P, i64, P],
+        "rmx_set_timing": [P, i32],
+        "rmx_reset_stats": [P],
+        "rmx_stats": [P, P, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.rmx_last_error.argtypes = [P]
+    lib.rmx_last_error.restype = ctypes.c_char_p
+    lib.rmx_version.restype = ctypes.c_int
+    lib.rmx_sm_target.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Context:
+    """An rmx_ctx bound to one CUDA device; calls enqueue on torch's current stream."""
+
+    def __init__(self, device: Optional[int] = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RmxError("no CUDA device: librmx has no CPU fallback")
+        self.lib = load_library()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            st = torch.cuda.current_stream().cuda_stream
+        rc = self.lib.rmx_create(ctypes.byref(self._h), self.device, ctypes.c_void_p(st))
+        if rc != RMX_OK:
+            raise RmxError(f"rmx_create failed (rc={rc})")
+
+    # ------------------------------------------------------------------ plumbing
+    def close(self):
+        if self._h:
+            self.lib.rmx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _bind_stream(self):
+        torch = _torch()
+        self.lib.rmx_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+
+    def _check(self, rc: int, what: str):
+        if rc != RMX_OK:
+            msg = self.lib.rmx_last_error(self._h)
+            raise RmxError(f"{what}: rc={rc}: {msg.decode() if msg else ''}")
+
+    def _dev(self, x, dtype):
+        torch = _torch()
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        t = x.to(device=f"cuda:{self.device}", dtype=dtype)
+        return t.contiguous()
+
+    def prepare_w(self, w):
+        """Device copy of w with an even leading dimension (TMA stride rule, rmx.h)."""
+        torch = _torch()
+        w = self._dev(w, torch.float64)
+        nch, nlev = w.shape
+        ldw = nlev + (nlev & 1)
+        if ldw != nlev or (w.data_ptr() % 16):
+            buf = torch.zeros((nch, ldw), dtype=torch.float64, device=w.device)
+            buf[:, :nlev] = w
+            w = buf
+        return w, nlev, ldw
+
+    def _status(self, status, ne):
+        torch = _torch()
+        if status is None:
+            return torch.zeros(ne, dtype=torch.int32, device=f"cuda:{self.device}")
+        return status
+
+    # ------------------------------------------------------------------ the three calls
+    def build_R(self, w, Ek, a: float, E, status=None, out=None):
+        """rmx_build_R: R[e] = (1/2a) W diag(1/(E_k - E_e)) W^T. Returns (R [ne,nch,nch], status)."""
+        torch = _torch()
+        self._bind_stream()
+        w, nlev, ldw = self.prepare_w(w)
+        Ek = self._dev(Ek, torch.float64)
+        E = self._dev(E, torch.float64)
+        nch, ne = w.shape[0], E.shape[0]
+        R = out if out is not None else torch.empty((ne, nch, nch), dtype=torch.float64, device=w.device)
+        status = self._status(status, ne)
+        self._check(self.lib.rmx_build_R(self._h, _ptr(w), ldw, _ptr(Ek), nch, nlev, float(a), _ptr(E),
+                                         ne, _ptr(R), _ptr(status)), "rmx_build_R")
+        return R, status
+
+    def match_K(self, R, F, G, Fp, Gp, a: float, n_open=None, status=None, out=None):
+        """rmx_match_K: K[e] = -(G - aRG')^{-1}(F - aRF'). Returns (K [ne,nch,nch], status)."""
+        torch = _torch()
+        self._bind_stream()
+        R = self._dev(R, torch.float64)
+        F, G, Fp, Gp = (self._dev(x, torch.float64) for x in (F, G, Fp, Gp))
+        ne, nch = R.shape[0], R.shape[1]
+        no = None if n_open is None else self._dev(n_open, torch.int32)
+        K = out if out is not None else torch.empty_like(R)
+        status = self._status(status, ne)
+        self._check(self.lib.rmx_match_K(self._h, _ptr(R), _ptr(F), _ptr(G), _ptr(Fp), _ptr(Gp),
+                                         float(a), nch, ne, _ptr(no), _ptr(K), _ptr(status)),
+                    "rmx_match_K")
+        return K, status
+
+    def collision_strength(self, K, n_open=None, status=None, want_T2: bool = True,
+                           want_rowsum: bool = True):
+        """rmx_collision_strength: |T|^2 with T = 2iK_oo(I - iK_oo)^{-1}.
+        Returns (T2 [ne,nch,nch] or None, rowsum [ne,nch] or None, status)."""
+        torch = _torch()
+        self._bind_stream()
+        K = self._dev(K, torch.float64)
+        ne, nch = K.shape[0], K.shape[1]
+        no = None if n_open is None else self._dev(n_open, torch.int32)
+        T2 = torch.empty_like(K) if want_T2 else None
+        rs = torch.empty((ne, nch), dtype=torch.float64, device=K.device) if want_rowsum else None
+        status = self._status(status, ne)
+        self._check(self.lib.rmx_collision_strength(self._h, _ptr(K), nch, ne, _ptr(no), _ptr(T2),
+                                                    _ptr(rs), _ptr(status)),
+                    "rmx_collision_strength")
+        return T2, rs, status
+
+    # ------------------------------------------------------------------ fused drivers
+    def sweep(self, w, Ek, a: float, E, F, G, Fp, Gp, n_open=None, batch: int = 0,
+              dump_idx: Optional[Sequence[int]] = None, status=None, rowsum=None, prepared=False):
+        """rmx_sweep: R -> K -> |T|^2 for all energies; returns dict with rowsum [ne,nch], status
+        [ne] and, for dump_idx, R/K/T2 [n_dump,nch,nch]."""
+        torch = _torch()
+        self._bind_stream()
+        if prepared:
+            nlev, ldw = int(prepared[0]), int(prepared[1])
+        else:
+            w, nlev, ldw = self.prepare_w(w)
+            Ek = self._dev(Ek, torch.float64)
+            E = self._dev(E, torch.float64)
+            F, G, Fp, Gp = (self._dev(x, torch.float64) for x in (F, G, Fp, Gp))
+            n_open = None if n_open is None else self._dev(n_open, torch.int32)
+        nch, ne = w.shape[0], E.shape[0]
+        dev = w.device
+        rs = rowsum if rowsum is not None else torch.empty((ne, nch), dtype=torch.float64, device=dev)
+        status = self._status(status, ne)
+        nd = 0 if dump_idx is None else len(dump_idx)
+        out = {"rowsum": rs, "status": status}
+        didx = None
+        Rd = Kd = T2d = None
+        if nd:
+            didx = np.ascontiguousarray(dump_idx, dtype=np.int64)
+            Rd = torch.empty((nd, nch, nch), dtype=torch.float64, device=dev)
+            Kd, T2d = torch.empty_like(Rd), torch.empty_like(Rd)
+            out.update(R=Rd, K=Kd, T2=T2d)
+        self._check(self.lib.rmx_sweep(
+            self._h, _ptr(w), ldw, _ptr(Ek), nch, nlev, float(a), _ptr(E), ne, _ptr(F), _ptr(G),
+            _ptr(Fp), _ptr(Gp), _ptr(n_open), int(batch),
+            didx.ctypes.data_as(ctypes.c_void_p) if nd else None, nd, _ptr(Rd), _ptr(Kd), _ptr(T2d),
+            _ptr(rs), _ptr(status)), "rmx_sweep")
+        return out
+
+    def sweep_host(self, w: np.ndarray, Ek: np.ndarray, a: float, E: np.ndarray, F: np.ndarray,
+                   G: np.ndarray, Fp: np.ndarray, Gp: np.ndarray, n_open: Optional[np.ndarray],
+                   batch: int = 0, rowsum: Optional[np.ndarray] = None,
+                   status: Optional[np.ndarray] = None):
+        """rmx_sweep_host: host arrays in, host rowsum/status out (copies inside the call).
+        Arrays should be pinned (see pinned_empty) for asynchronous copies.
+        Returns (rowsum, status, h2d_bytes, d2h_bytes)."""
+        self._bind_stream()
+        nch, ldw = w.shape
+        nlev = Ek.shape[0]
+        ne = E.shape[0]
+        if rowsum is None:
+            rowsum = np.empty((ne, nch))
+        if status is None:
+            status = np.empty(ne, dtype=np.int32)
+        h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
+        P = lambda x: None if x is None else x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        self._check(self.lib.rmx_sweep_host(
+            self._h, P(w), ldw, P(Ek), nch, nlev, float(a), P(E), ne, P(F), P(G), P(Fp), P(Gp),
+            P(n_open), int(batch), P(rowsum), P(status), ctypes.byref(h2d), ctypes.byref(d2h)),
+            "rmx_sweep_host")
+        return rowsum, status, h2d.value, d2h.value
+
+    # ------------------------------------------------------------------ instrumentation
+    def set_timing(self, on: bool = True):
+        self._check(self.lib.rmx_set_timing(self._h, 1 if on else 0), "rmx_set_timing")
+
+    def reset_stats(self):
+        self._check(self.lib.rmx_reset_stats(self._h), "rmx_reset_stats")
+
+    def stats(self):
+        ms = (ctypes.c_double * 4)()
+        cnt = (ctypes.c_int64 * 4)()
+        tot = ctypes.c_int64()
+        self._check(self.lib.rmx_stats(self._h, ms, cnt, ctypes.byref(tot)), "rmx_stats")
+        return {KID_NAMES[k]: (ms[k], cnt[k]) for k in range(4)} | {"launches": tot.value}
+
+    def sync(self, status=None):
+        n_bad = ctypes.c_int64()
+        ne = 0 if status is None else status.numel()
+        self._check(self.lib.rmx_sync(self._h, _ptr(status), ne, ctypes.byref(n_bad)), "rmx_sync")
+        return n_bad.value
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array backed by pinned (page-locked) host memory via torch."""
+    torch = _torch()
+    tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int64: torch.int64}[np.dtype(dtype).type]
+    t = torch.empty(shape, dtype=tdt, pin_memory=True)
+    _pinned_keepalive.append(t)  # the numpy view does not own the pinned storage
+    return t.numpy()
+
+
+_pinned_keepalive = []
+
+
+_default_ctx = {}
+
+
+def _ctx() -> Context:
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _default_ctx:
+        _default_ctx[dev] = Context(dev)
+    return _default_ctx[dev]
+
+
+# module-level functions with the C-ABI names (argument marshalling only)
+def rmx_build_R(w, Ek, a, E, status=None):
+    return _ctx().build_R(w, Ek, a, E, status=status)
+
+
+def rmx_match_K(R, F, G, Fp, Gp, a, n_open=None, status=None):
+    return _ctx().match_K(R, F, G, Fp, Gp, a, n_open=n_open, status=status)
+
+
+def rmx_collision_strength(K, n_open=None, status=None):
+    return _ctx().collision_strength(K, n_open=n_open, status=status)
+
+
+def rmx_sweep(w, Ek, a, E, F, G, Fp, Gp, n_open=None, batch=0, dump_idx=None):
+    return _ctx().sweep(w, Ek, a, E, F, G, Fp, Gp, n_open=n_open, batch=batch, dump_idx=dump_idx)

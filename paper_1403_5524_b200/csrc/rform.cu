@@ -1,0 +1,360 @@
+// rform.cu - S1+S2 of the sweep: R_ij(E) = (1/2a) sum_k w_ik w_jk / (E_k - E)
+// (§6 Eq. 1-2 "R = X x Y" with X_ik = w_ik/(E - E_k), Y = w_kj; written in the
+// north_star convention of BASELINE.json:5). B200 design:
+//   * one CTA per (energy, upper-triangle tile pair (I <= J)); grid enumerates tile pairs fastest so
+//     the CTAs resident at any time stream the same W k-slabs through L2 (W read from HBM ~once per
+//     energy wave instead of once per tile pair);
+//   * a producer warp issues 2D TMA loads (SWIZZLE_128B, 16 doubles x BM rows per box) of the W rows of
+//     tile I and tile J into a STAGES-deep mbarrier ring, and computes the stage's denominators
+//     d_k = 1/(E_k - E) on chip (X of Eq. 2 is never materialised) plus the pole guard;
+//   * consumer warps run FP64 tensor-core MMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4, the only FP64
+//     MMA on sm_100a; tcgen05 has no f64 kind), scaling the A fragment by d_k in registers;
+//   * fragment rows are permuted inside each 8-row group (g -> (g>>1) + 4(g&1)) so that the 16-byte
+//     fragment loads from the 128B-swizzled tiles are bank-conflict free;
+//   * epilogue scales by 1/2a and stores the tile and its mirror image: R is bitwise symmetric.
+#include "rmx_common.cuh"
+#include "rmx_internal.h"
+
+namespace rmx {
+
+template <int BM_, int WM_, int WN_, int STAGES_>
+struct RformCfg {
+  static constexpr int BM = BM_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BK = 32;    // k per pipeline stage
+  static constexpr int BOXK = 16;  // doubles per TMA box row (128 B = swizzle span)
+  static constexpr int NCW = WM * WN;
+  static constexpr int NT = (NCW + 1) * 32;
+  static constexpr int WTM = BM / WM, WTN = BM / WN;
+  static constexpr int MI = WTM / 8, NI = WTN / 8;
+  static constexpr int BOX_BYTES = BM * BOXK * 8;
+  static constexpr int OP_BYTES = 2 * BOX_BYTES;   // one operand, one stage
+  static constexpr int STAGE_BYTES = 2 * OP_BYTES;  // tile I + tile J
+  static constexpr int SMEM_BYTES =
+      1024 + STAGES * STAGE_BYTES + STAGES * BK * 8 + 2 * STAGES * 8 + 16;
+  static_assert(BOX_BYTES % 1024 == 0, "swizzle-128B boxes must stay 1024-byte aligned");
+};
+
+__device__ __forceinline__ int frag_row_perm(int g) { return (g >> 1) + 4 * (g & 1); }
+
+// Decode upper-triangle tile pair index -> (ti, tj), ti <= tj, row-major over ti.
+__device__ __forceinline__ void decode_pair(int p, int ntiles, int &ti, int &tj) {
+  ti = 0;
+  while (p >= ntiles - ti) {
+    p -= ntiles - ti;
+    ++ti;
+  }
+  tj = ti + p;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, 1)
+    rform_dmma_kernel(const __grid_constant__ CUtensorMap wmap, const double *__restrict__ Ek,
+                      const double *__restrict__ E, int nch, int nlev, int ntiles, int npairs,
+                      double inv2a, double *__restrict__ R, int32_t *__restrict__ status) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  double *dsm = reinterpret_cast<double *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
+  uint64_t *empty = full + C::STAGES;
+  int *pole_flag = reinterpret_cast<int *>(empty + C::STAGES);
+
+  const int pair = blockIdx.x % npairs;
+  const int64_t e = blockIdx.x / npairs;
+  int ti, tj;
+  decode_pair(pair, ntiles, ti, tj);
+  const bool diag = (ti == tj);
+  const double Ee = E[e];
+  const int nk = (nlev + C::BK - 1) / C::BK;
+  const int warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    *pole_flag = 0;
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {
+    // ===================== producer warp: TMA + denominators =====================
+    if (lane == 0) tma_prefetch_desc(&wmap);
+    int found_pole = 0;
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % C::STAGES;
+      if (kt >= C::STAGES) mbar_wait(&empty[s], ((kt / C::STAGES) - 1) & 1);
+      const int k = kt * C::BK + lane;  // BK == 32 == warp size
+      double dv = 0.0;
+      if (k < nlev) {
+        const double diff = __ldg(Ek + k) - Ee;
+        if (fabs(diff) < kPoleGuard) found_pole = 1;
+        dv = 1.0 / diff;
+      }
+      dsm[s * C::BK + lane] = dv;
+      if (found_pole) *pole_flag = 1;
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bytes = diag ? C::OP_BYTES : 2 * C::OP_BYTES;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+        const int k0 = kt * C::BK;
+        tma_load_2d(base, &wmap, &full[s], k0, ti * C::BM);
+        tma_load_2d(base + C::BOX_BYTES, &wmap, &full[s], k0 + C::BOXK, ti * C::BM);
+        if (!diag) {
+          tma_load_2d(base + C::OP_BYTES, &wmap, &full[s], k0, tj * C::BM);
+          tma_load_2d(base + C::OP_BYTES + C::BOX_BYTES, &wmap, &full[s], k0 + C::BOXK,
+                      tj * C::BM);
+        }
+      }
+    }
+    return;
+  }
+
+  // ===================== consumer warps: FP64 DMMA =====================
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  const int g = lane >> 2, t = lane & 3;
+  const int prow = frag_row_perm(g);
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+  // byte offsets of this lane's fragment rows inside a box (row * 128); swizzle xor = prow
+  uint32_t arow[C::MI], brow[C::NI];
+#pragma unroll
+  for (int mi = 0; mi < C::MI; ++mi) arow[mi] = (wm * C::WTM + mi * 8 + prow) * 128;
+#pragma unroll
+  for (int ni = 0; ni < C::NI; ++ni) brow[ni] = (wn * C::WTN + ni * 8 + prow) * 128;
+
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % C::STAGES;
+    mbar_wait(&full[s], (kt / C::STAGES) & 1);
+    const uint32_t abase = smem_u32(smem + s * C::STAGE_BYTES);
+    const uint32_t bbase = diag ? abase : abase + C::OP_BYTES;
+    const uint32_t dbase = smem_u32(dsm + s * C::BK);
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        // this lane's two k values: k = kb*16 + kk*8 + 2t + {0,1}; 16-byte chunk c = kk*4 + t
+        const uint32_t chunk = static_cast<uint32_t>(((kk * 4 + t) ^ prow) << 4);
+        double d0, d1;
+        lds128(d0, d1, dbase + (kb * 16 + kk * 8 + 2 * t) * 8);
+        double a[C::MI][2], b[C::NI][2];
+#pragma unroll
+        for (int mi = 0; mi < C::MI; ++mi) {
+          lds128(a[mi][0], a[mi][1], abase + kb * C::BOX_BYTES + arow[mi] + chunk);
+          a[mi][0] *= d0;
+          a[mi][1] *= d1;
+        }
+#pragma unroll
+        for (int ni = 0; ni < C::NI; ++ni)
+          lds128(b[ni][0], b[ni][1], bbase + kb * C::BOX_BYTES + brow[ni] + chunk);
+#pragma unroll
+        for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < C::NI; ++ni) {
+            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][0], b[ni][0]);
+            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][1], b[ni][1]);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ===================== epilogue: scale, store tile + mirror =====================
+  const bool pole = (*reinterpret_cast<volatile int *>(pole_flag)) != 0;
+  if (pole && pair == 0 && warp == 0 && lane == 0) set_status(status, e, RMX_E_POLE);
+  double *Re = R + e * static_cast<int64_t>(nch) * nch;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+#pragma unroll
+  for (int mi = 0; mi < C::MI; ++mi) {
+    const int row = ti * C::BM + wm * C::WTM + mi * 8 + prow;
+    if (row >= nch) continue;
+#pragma unroll
+    for (int ni = 0; ni < C::NI; ++ni) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = tj * C::BM + wn * C::WTN + ni * 8 + t + 4 * h;
+        if (col >= nch) continue;
+        if (diag && row > col) continue;  // lower half of a diagonal tile comes from its mirror
+        const double v = pole ? nan : acc[mi][ni][h] * inv2a;
+        Re[static_cast<int64_t>(row) * nch + col] = v;
+        if (row != col) Re[static_cast<int64_t>(col) * nch + row] = v;
+      }
+    }
+  }
+}
+
+// Small-channel path (nch <= 32, e.g. BASELINE.json:7 'tiny'): one CTA per energy, each thread owns
+// up to 3 upper-triangle entries (nch(nch+1)/2 <= 528 <= 3*256), denominators staged through shared
+// memory in chunks. Launch-bound by construction (SURVEY.md §7 hard part 8).
+__global__ void __launch_bounds__(256) rform_small_kernel(const double *__restrict__ w, int64_t ldw,
+                                                          const double *__restrict__ Ek,
+                                                          const double *__restrict__ E, int nch,
+                                                          int nlev, double inv2a,
+                                                          double *__restrict__ R,
+                                                          int32_t *__restrict__ status) {
+  constexpr int PPT = 3;
+  __shared__ double ds[1024];
+  __shared__ int pole;
+  const int64_t e = blockIdx.x;
+  const double Ee = E[e];
+  if (threadIdx.x == 0) pole = 0;
+  const int npair = nch * (nch + 1) / 2;
+  int pi[PPT], pj[PPT];
+  double s[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    pi[q] = -1;
+    pj[q] = -1;
+    s[q] = 0.0;
+    int p = threadIdx.x + q * blockDim.x;
+    if (p < npair) {
+      int i = 0;
+      while (p >= nch - i) {
+        p -= nch - i;
+        ++i;
+      }
+      pi[q] = i;
+      pj[q] = i + p;
+    }
+  }
+  for (int k0 = 0; k0 < nlev; k0 += 1024) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < 1024; k += blockDim.x) {
+      double dv = 0.0;
+      if (k0 + k < nlev) {
+        const double diff = Ek[k0 + k] - Ee;
+        if (fabs(diff) < kPoleGuard) pole = 1;
+        dv = 1.0 / diff;
+      }
+      ds[k] = dv;
+    }
+    __syncthreads();
+    const int kn = min(1024, nlev - k0);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      if (pi[q] < 0) continue;
+      const double *wi = w + pi[q] * ldw + k0, *wj = w + pj[q] * ldw + k0;
+      double acc = s[q];
+      for (int k = 0; k < kn; ++k) acc = fma(wi[k] * ds[k], wj[k], acc);
+      s[q] = acc;
+    }
+  }
+  __syncthreads();
+  double *Re = R + e * static_cast<int64_t>(nch) * nch;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    if (pi[q] < 0) continue;
+    const double v = pole ? nan : s[q] * inv2a;
+    Re[pi[q] * nch + pj[q]] = v;
+    Re[pj[q] * nch + pi[q]] = v;
+  }
+  if (pole && threadIdx.x == 0) set_status(status, e, RMX_E_POLE);
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                      const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                      const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+template <class C>
+static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *Ek, int nch,
+                                    int nlev, double a, const double *E, int64_t ne, double *R,
+                                    int32_t *status, cudaStream_t st, std::string &err) {
+  PFN_encodeTiled_t enc = get_encode_fn();
+  if (!enc) {
+    err = "cuTensorMapEncodeTiled unavailable";
+    return cudaErrorNotSupported;
+  }
+  CUtensorMap map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(nlev), static_cast<cuuint64_t>(nch)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw) * 8};
+  cuuint32_t box[2] = {C::BOXK, C::BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(w), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) + ")";
+    return cudaErrorInvalidValue;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t ce = cudaFuncSetAttribute(rform_dmma_kernel<C>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          C::SMEM_BYTES);
+    if (ce != cudaSuccess) return ce;
+    attr_set = true;
+  }
+  const int ntiles = (nch + C::BM - 1) / C::BM;
+  const int npairs = ntiles * (ntiles + 1) / 2;
+  const double inv2a = 1.0 / (2.0 * a);
+  // grid.x <= 2^31-1: chunk the energies
+  const int64_t max_e = (static_cast<int64_t>(1) << 30) / npairs;
+  for (int64_t e0 = 0; e0 < ne; e0 += max_e) {
+    const int64_t n = (ne - e0 < max_e) ? ne - e0 : max_e;
+    rform_dmma_kernel<C><<<static_cast<unsigned>(n * npairs), C::NT, C::SMEM_BYTES, st>>>(
+        map, Ek, E + e0, nch, nlev, ntiles, npairs, inv2a,
+        R + e0 * static_cast<int64_t>(nch) * nch, status ? status + e0 : nullptr);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return ce;
+  }
+  return cudaSuccess;
+}
+
+using Rform128 = RformCfg<128, 4, 2, 3>;
+using Rform64 = RformCfg<64, 2, 2, 3>;
+
+int rform_tile_for(int64_t nch) {
+  if (nch <= 32) return 0;
+  if (nch <= 96) return 64;
+  // pick the tile that wastes the fewest MMA lanes on ragged / diagonal tiles
+  auto waste = [&](int bm) {
+    int64_t nt = (nch + bm - 1) / bm;
+    double computed = static_cast<double>(nt * (nt + 1) / 2) * bm * bm;
+    return computed / (0.5 * nch * (nch + 1));
+  };
+  return waste(128) <= 1.08 * waste(64) ? 128 : 64;
+}
+
+cudaError_t launch_rform(const double *w, int64_t ldw, const double *Ek, int64_t nch, int64_t nlev,
+                         double a, const double *E, int64_t ne, double *R, int32_t *status,
+                         cudaStream_t st, std::string &err) {
+  const int bm = rform_tile_for(nch);
+  if (bm == 0) {
+    rform_small_kernel<<<static_cast<unsigned>(ne), 256, 0, st>>>(
+        w, ldw, Ek, E, static_cast<int>(nch), static_cast<int>(nlev), 1.0 / (2.0 * a), R, status);
+    return cudaGetLastError();
+  }
+  if (bm == 64)
+    return launch_rform_cfg<Rform64>(w, ldw, Ek, static_cast<int>(nch), static_cast<int>(nlev), a,
+                                     E, ne, R, status, st, err);
+  return launch_rform_cfg<Rform128>(w, ldw, Ek, static_cast<int>(nch), static_cast<int>(nlev), a,
+                                    E, ne, R, status, st, err);
+}
+
+}  // namespace rmx

@@ -1,0 +1,425 @@
+// rmx_api.cu - the C ABI of librmx (include/rmx.h): context, argument validation, workspace,
+// the streaming sweep driver and launch instrumentation. All arithmetic of the method lives in
+// rform.cu / match.cu / tepi.cu; this file only validates, allocates and launches.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rmx_internal.h"
+
+using namespace rmx;
+
+struct PendingTiming {
+  int kid;
+  cudaEvent_t a, b;
+};
+
+struct rmx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  std::string err;
+  cudaError_t sticky = cudaSuccess;
+  // linear-algebra workspace (match / tepi slots)
+  double *ws = nullptr;
+  size_t ws_bytes = 0;
+  // sweep batch buffer (R, then K in place)
+  double *rbuf = nullptr;
+  size_t rbuf_bytes = 0;
+  // device mirrors for rmx_sweep_host
+  struct Dev {
+    void *p = nullptr;
+    size_t bytes = 0;
+  } dw, dEk, dE, dF, dG, dFp, dGp, dno, drs, dst;
+  // instrumentation
+  bool timing = false;
+  std::vector<cudaEvent_t> free_events;
+  std::vector<PendingTiming> pending;
+  double ms[RMX_NKID] = {0, 0, 0, 0};
+  int64_t cnt[RMX_NKID] = {0, 0, 0, 0};
+  int64_t launches = 0;
+};
+
+namespace {
+
+rmx_rc fail(rmx_ctx *c, rmx_rc rc, const std::string &msg) {
+  if (c) c->err = msg;
+  return rc;
+}
+
+rmx_rc cuda_fail(rmx_ctx *c, cudaError_t e, const char *where) {
+  if (c) {
+    c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    c->sticky = e;
+  }
+  return RMX_ECUDA;
+}
+
+cudaEvent_t get_event(rmx_ctx *c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one launcher call with events when timing is on; counts kernel launches.
+template <class F>
+cudaError_t timed(rmx_ctx *c, int kid, int nlaunch, F &&f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) {
+    a = get_event(c);
+    b = get_event(c);
+    cudaEventRecord(a, c->stream);
+  }
+  cudaError_t e = f();
+  if (c->timing) {
+    cudaEventRecord(b, c->stream);
+    c->pending.push_back({kid, a, b});
+  }
+  c->launches += nlaunch;
+  c->cnt[kid] += nlaunch;
+  return e;
+}
+
+void drain_timing(rmx_ctx *c) {
+  for (auto &p : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(p.b);
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    c->ms[p.kid] += ms;
+    c->free_events.push_back(p.a);
+    c->free_events.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
+rmx_rc grow(rmx_ctx *c, void **p, size_t *have, size_t need) {
+  if (need <= *have) return RMX_OK;
+  if (*p) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+  }
+  need = std::max<size_t>(need, 256);
+  cudaError_t e = cudaMalloc(p, need);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, RMX_ENOMEM, "cudaMalloc(" + std::to_string(need) + " B) failed");
+  }
+  *have = need;
+  return RMX_OK;
+}
+
+rmx_rc grow(rmx_ctx *c, rmx_ctx::Dev &d, size_t need) { return grow(c, &d.p, &d.bytes, need); }
+
+int64_t ws_slots_for(const rmx_ctx *c, int64_t ne) {
+  return std::min<int64_t>(ne, 2 * static_cast<int64_t>(c->nsm));
+}
+
+rmx_rc ensure_ws(rmx_ctx *c, int64_t nch, int64_t slots) {
+  const int64_t per = std::max(match_ws_doubles_per_slot(nch), tepi_ws_doubles_per_slot(nch));
+  return grow(c, reinterpret_cast<void **>(&c->ws), &c->ws_bytes,
+              static_cast<size_t>(per * slots) * sizeof(double));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+rmx_rc check_sticky(rmx_ctx *c) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, "pending CUDA error");
+  return RMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rmx_version(void) { return 100; }
+int rmx_sm_target(void) { return 100; }
+
+rmx_rc rmx_create(rmx_ctx **ctx, int device, void *stream) {
+  if (!ctx) return RMX_EINVAL;
+  *ctx = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return RMX_EINVAL;
+  }
+  rmx_ctx *c = new rmx_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  cudaSetDevice(device);
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  *ctx = c;
+  return RMX_OK;
+}
+
+rmx_rc rmx_destroy(rmx_ctx *c) {
+  if (!c) return RMX_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  drain_timing(c);
+  for (auto e : c->free_events) cudaEventDestroy(e);
+  cudaFree(c->ws);
+  cudaFree(c->rbuf);
+  for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
+                  &c->dst})
+    cudaFree(d->p);
+  delete c;
+  return RMX_OK;
+}
+
+rmx_rc rmx_set_stream(rmx_ctx *c, void *stream) {
+  if (!c) return RMX_EINVAL;
+  c->stream = static_cast<cudaStream_t>(stream);
+  return RMX_OK;
+}
+
+const char *rmx_last_error(const rmx_ctx *c) { return c ? c->err.c_str() : "null ctx"; }
+
+rmx_rc rmx_build_R(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                   int64_t nlev, double a, const double *E, int64_t ne, double *R,
+                   int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!w || !Ek || !E || !R) return fail(c, RMX_EINVAL, "rmx_build_R: null pointer");
+  if (nch < 1 || nlev < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_build_R: sizes must be >= 1");
+  if (nch > (1 << 20) || nlev > (1 << 30)) return fail(c, RMX_EINVAL, "rmx_build_R: size too large");
+  if (!(a > 0.0)) return fail(c, RMX_EINVAL, "rmx_build_R: a must be > 0");
+  if (ldw < nlev || (ldw & 1) || !aligned16(w))
+    return fail(c, RMX_EINVAL, "rmx_build_R: ldw must be >= nlev and even, w 16-byte aligned");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  std::string err;
+  cudaError_t e = timed(c, RMX_KID_RFORM, 1, [&] {
+    return launch_rform(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->stream, err);
+  });
+  if (e != cudaSuccess) {
+    if (!err.empty()) return fail(c, RMX_ECUDA, "rmx_build_R: " + err);
+    return cuda_fail(c, e, "rmx_build_R");
+  }
+  return RMX_OK;
+}
+
+rmx_rc rmx_match_K(rmx_ctx *c, const double *R, const double *F, const double *G,
+                   const double *Fp, const double *Gp, double a, int64_t nch, int64_t ne,
+                   const int32_t *n_open, double *K, int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!R || !F || !G || !Fp || !Gp || !K) return fail(c, RMX_EINVAL, "rmx_match_K: null pointer");
+  if (nch < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_match_K: sizes must be >= 1");
+  if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_match_K: nch too large");
+  if (!(a > 0.0)) return fail(c, RMX_EINVAL, "rmx_match_K: a must be > 0");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  const int64_t slots = ws_slots_for(c, ne);
+  rmx_rc rc = ensure_ws(c, nch, slots);
+  if (rc != RMX_OK) return rc;
+  cudaError_t e = timed(c, RMX_KID_MATCH, 1, [&] {
+    return launch_match(R, F, G, Fp, Gp, a, nch, ne, n_open, K, c->ws, slots, status, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_match_K");
+  return RMX_OK;
+}
+
+rmx_rc rmx_collision_strength(rmx_ctx *c, const double *K, int64_t nch, int64_t ne,
+                              const int32_t *n_open, double *T2, double *rowsum,
+                              int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!K) return fail(c, RMX_EINVAL, "rmx_collision_strength: null K");
+  if (nch < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_collision_strength: sizes must be >= 1");
+  if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_collision_strength: nch too large");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  const int64_t slots = ws_slots_for(c, ne);
+  rmx_rc rc = ensure_ws(c, nch, slots);
+  if (rc != RMX_OK) return rc;
+  cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, c->ws, slots,
+                       status, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_collision_strength");
+  return RMX_OK;
+}
+
+static int64_t default_batch(const rmx_ctx *c, int64_t nch, int64_t ne) {
+  const int64_t unit = 2 * static_cast<int64_t>(c->nsm);
+  const int64_t budget = static_cast<int64_t>(8) << 30;  // bytes for the R/K batch buffer
+  int64_t b = budget / (nch * nch * 8);
+  b = std::max<int64_t>(unit, (b / unit) * unit);
+  return std::min<int64_t>(b, ne);
+}
+
+rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                 int64_t nlev, double a, const double *E, int64_t ne, const double *F,
+                 const double *G, const double *Fp, const double *Gp, const int32_t *n_open,
+                 int64_t batch, const int64_t *dump_idx, int64_t n_dump, double *R_d,
+                 double *K_d, double *T2_d, double *rowsum, int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!w || !Ek || !E || !F || !G || !Fp || !Gp || !rowsum)
+    return fail(c, RMX_EINVAL, "rmx_sweep: null pointer");
+  if (nch < 1 || nlev < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_sweep: sizes must be >= 1");
+  if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_sweep: nch too large");
+  if (!(a > 0.0)) return fail(c, RMX_EINVAL, "rmx_sweep: a must be > 0");
+  if (ldw < nlev || (ldw & 1) || !aligned16(w))
+    return fail(c, RMX_EINVAL, "rmx_sweep: ldw must be >= nlev and even, w 16-byte aligned");
+  if (n_dump < 0 || (n_dump > 0 && !dump_idx)) return fail(c, RMX_EINVAL, "rmx_sweep: bad dump list");
+  for (int64_t d = 0; d < n_dump; ++d)
+    if (dump_idx[d] < 0 || dump_idx[d] >= ne) return fail(c, RMX_EINVAL, "rmx_sweep: dump index out of range");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  if (batch <= 0) batch = default_batch(c, nch, ne);
+  batch = std::min(batch, ne);
+  const int64_t slots = ws_slots_for(c, batch);
+  rmx_rc rc = ensure_ws(c, nch, slots);
+  if (rc != RMX_OK) return rc;
+  const size_t mat = static_cast<size_t>(nch) * nch;
+  rc = grow(c, reinterpret_cast<void **>(&c->rbuf), &c->rbuf_bytes,
+            static_cast<size_t>(batch) * mat * sizeof(double));
+  if (rc != RMX_OK) return rc;
+  double *rb = c->rbuf;
+  std::string err;
+  for (int64_t b0 = 0; b0 < ne; b0 += batch) {
+    const int64_t nb = std::min(batch, ne - b0);
+    int32_t *stb = status ? status + b0 : nullptr;
+    const int32_t *nob = n_open ? n_open + b0 : nullptr;
+    cudaError_t e = timed(c, RMX_KID_RFORM, 1, [&] {
+      return launch_rform(w, ldw, Ek, nch, nlev, a, E + b0, nb, rb, stb, c->stream, err);
+    });
+    if (e != cudaSuccess) return err.empty() ? cuda_fail(c, e, "rmx_sweep/R") : fail(c, RMX_ECUDA, err);
+    for (int64_t d = 0; d < n_dump; ++d)
+      if (R_d && dump_idx[d] >= b0 && dump_idx[d] < b0 + nb)
+        cudaMemcpyAsync(R_d + d * mat, rb + (dump_idx[d] - b0) * mat, mat * sizeof(double),
+                        cudaMemcpyDeviceToDevice, c->stream);
+    e = timed(c, RMX_KID_MATCH, 1, [&] {
+      return launch_match(rb, F + b0 * nch, G + b0 * nch, Fp + b0 * nch, Gp + b0 * nch, a, nch, nb,
+                          nob, rb, c->ws, slots, stb, c->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/K");
+    for (int64_t d = 0; d < n_dump; ++d) {
+      const int64_t l = dump_idx[d] - b0;
+      if (l < 0 || l >= nb) continue;
+      if (K_d)
+        cudaMemcpyAsync(K_d + d * mat, rb + l * mat, mat * sizeof(double),
+                        cudaMemcpyDeviceToDevice, c->stream);
+      if (T2_d) {
+        e = timed(c, RMX_KID_TEPI, 1, [&] {
+          return launch_tepi(rb + l * mat, nch, mat, nch, 1, nob ? nob + l : nullptr, T2_d + d * mat,
+                             nullptr, nullptr, c->ws, 1, nullptr, c->stream);
+        });
+        if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T dump");
+      }
+    }
+    e = timed(c, RMX_KID_TEPI, 1, [&] {
+      return launch_tepi(rb, nch, mat, nch, nb, nob, nullptr, nullptr, rowsum + b0 * nch, c->ws,
+                         slots, stb, c->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T");
+  }
+  return RMX_OK;
+}
+
+rmx_rc rmx_sweep_host(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                      int64_t nlev, double a, const double *E, int64_t ne, const double *F,
+                      const double *G, const double *Fp, const double *Gp, const int32_t *n_open,
+                      int64_t batch, double *rowsum, int32_t *status, int64_t *h2d_bytes,
+                      int64_t *d2h_bytes) {
+  if (!c) return RMX_EINVAL;
+  if (!w || !Ek || !E || !F || !G || !Fp || !Gp || !rowsum || !status)
+    return fail(c, RMX_EINVAL, "rmx_sweep_host: null pointer");
+  if (nch < 1 || nlev < 1 || ne < 1 || ldw < nlev || (ldw & 1))
+    return fail(c, RMX_EINVAL, "rmx_sweep_host: bad sizes / ldw");
+  cudaSetDevice(c->device);
+  const size_t bw = sizeof(double) * nch * ldw, bek = sizeof(double) * nlev,
+               be = sizeof(double) * ne, bf = sizeof(double) * ne * nch,
+               bno = sizeof(int32_t) * ne;
+  rmx_rc rc;
+  if ((rc = grow(c, c->dw, bw)) || (rc = grow(c, c->dEk, bek)) || (rc = grow(c, c->dE, be)) ||
+      (rc = grow(c, c->dF, bf)) || (rc = grow(c, c->dG, bf)) || (rc = grow(c, c->dFp, bf)) ||
+      (rc = grow(c, c->dGp, bf)) || (rc = grow(c, c->dno, bno)) || (rc = grow(c, c->drs, bf)) ||
+      (rc = grow(c, c->dst, bno)))
+    return rc;
+  auto h2d = [&](void *dst, const void *src, size_t n) {
+    return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->stream);
+  };
+  cudaError_t e = cudaSuccess;
+  e = e ? e : h2d(c->dw.p, w, bw);
+  e = e ? e : h2d(c->dEk.p, Ek, bek);
+  e = e ? e : h2d(c->dE.p, E, be);
+  e = e ? e : h2d(c->dF.p, F, bf);
+  e = e ? e : h2d(c->dG.p, G, bf);
+  e = e ? e : h2d(c->dFp.p, Fp, bf);
+  e = e ? e : h2d(c->dGp.p, Gp, bf);
+  if (n_open) e = e ? e : h2d(c->dno.p, n_open, bno);
+  e = e ? e : cudaMemsetAsync(c->dst.p, 0, bno, c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep_host/h2d");
+  rc = rmx_sweep(c, static_cast<double *>(c->dw.p), ldw, static_cast<double *>(c->dEk.p), nch, nlev,
+                 a, static_cast<double *>(c->dE.p), ne, static_cast<double *>(c->dF.p),
+                 static_cast<double *>(c->dG.p), static_cast<double *>(c->dFp.p),
+                 static_cast<double *>(c->dGp.p),
+                 n_open ? static_cast<int32_t *>(c->dno.p) : nullptr, batch, nullptr, 0, nullptr,
+                 nullptr, nullptr, static_cast<double *>(c->drs.p),
+                 static_cast<int32_t *>(c->dst.p));
+  if (rc != RMX_OK) return rc;
+  e = cudaMemcpyAsync(rowsum, c->drs.p, bf, cudaMemcpyDeviceToHost, c->stream);
+  e = e ? e : cudaMemcpyAsync(status, c->dst.p, bno, cudaMemcpyDeviceToHost, c->stream);
+  e = e ? e : cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep_host/d2h");
+  if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(bw + bek + be + 4 * bf + (n_open ? bno : 0));
+  if (d2h_bytes) *d2h_bytes = static_cast<int64_t>(bf + bno);
+  return RMX_OK;
+}
+
+rmx_rc rmx_sync(rmx_ctx *c, const int32_t *status, int64_t ne, int64_t *n_bad) {
+  if (!c) return RMX_EINVAL;
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sync");
+  if (c->sticky != cudaSuccess) return RMX_ECUDA;
+  if (n_bad) {
+    *n_bad = 0;
+    if (status && ne > 0) {
+      std::vector<int32_t> h(static_cast<size_t>(ne));
+      e = cudaMemcpy(h.data(), status, sizeof(int32_t) * ne, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sync/status");
+      for (auto s : h) *n_bad += (s != 0);
+    }
+  }
+  return RMX_OK;
+}
+
+rmx_rc rmx_set_timing(rmx_ctx *c, int enable) {
+  if (!c) return RMX_EINVAL;
+  c->timing = enable != 0;
+  return RMX_OK;
+}
+
+rmx_rc rmx_reset_stats(rmx_ctx *c) {
+  if (!c) return RMX_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  drain_timing(c);
+  for (int k = 0; k < RMX_NKID; ++k) {
+    c->ms[k] = 0;
+    c->cnt[k] = 0;
+  }
+  c->launches = 0;
+  return RMX_OK;
+}
+
+rmx_rc rmx_stats(rmx_ctx *c, double *ms, int64_t *launches, int64_t *total) {
+  if (!c) return RMX_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  drain_timing(c);
+  for (int k = 0; k < RMX_NKID; ++k) {
+    if (ms) ms[k] = c->ms[k];
+    if (launches) launches[k] = c->cnt[k];
+  }
+  if (total) *total = c->launches;
+  return RMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// tepi.cu - S5 of the sweep: T = 2i K_oo (I - i K_oo)^{-1} and |T_ij|^2 (BASELINE.json:5).
+// Real SPD route (reading T2): with K_oo symmetric,
+//   (I - iK)^{-1} = (I + iK)(I + K^2)^{-1}  =>  T = 2iX - 2KX,  X = (I + K K^T)^{-1} K
+// so Re T = -2P, Im T = 2X with P = K X, and |T_ij|^2 = 4 (X_ij^2 + P_ij^2). Per energy (one CTA,
+// persistent over energies): S = I + K K^T (lower, DMMA GEMM), blocked Cholesky S = L L^T, two
+// blocked triangular solves for X, P = K X (DMMA GEMM), then an epilogue pass writing |T|^2
+// (optional) and the row sums sum_j |T_ij|^2 in a fixed order (deterministic).
+// |T|^2 and the row sums are invariant under K -> -K, so the sweep may pass Y = -K directly.
+#include "cta_la.cuh"
+#include "rmx_internal.h"
+
+namespace rmx {
+
+using namespace la;
+
+struct TepiSmem {
+  double gemm[GEMM_SMEM_DOUBLES];
+  double tri[TRI_SMEM_DOUBLES];
+};
+
+__global__ void __launch_bounds__(NT, 1)
+    tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
+                const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
+                double *rowsum, double *ws, int64_t ws_slot, int ldo, int32_t *status) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  TepiSmem &sm = *reinterpret_cast<TepiSmem *>(smem_raw);
+  double *S = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;  // o x ldo; later holds P
+  double *X = S + static_cast<int64_t>(n) * ldo;                // o x ldo
+
+  for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
+    int o = n_open ? n_open[e] : n;
+    o = o < 0 ? 0 : (o > n ? n : o);
+    const double *Ke = K + e * kstride;
+    double *T2e = nullptr;
+    if (T2) {
+      const int64_t slot = t2_slot ? t2_slot[e] : e;
+      if (slot >= 0) T2e = T2 + slot * static_cast<int64_t>(n) * n;
+    }
+    int bad = 0;
+    if (o > 0) {
+      // S = I + K_oo K_oo^T (lower tiles)
+      gemm<true, true>(o, o, o, Ke, ldk, Ke, ldk, true, sm.gemm, EpiStore{S, ldo, 1.0});
+      // blocked Cholesky, lower
+      for (int p0 = 0; p0 < o; p0 += PB) {
+        const int bw = min(PB, o - p0);
+        bad |= chol_diag(S, ldo, p0, bw, sm.tri);
+        if (p0 + bw < o) {
+          trsm_rows_lt(sm.tri, bw, S, ldo, p0, p0 + bw, o);
+          const int m2 = o - p0 - bw;
+          const double *L21 = S + static_cast<int64_t>(p0 + bw) * ldo + p0;
+          double *C = S + static_cast<int64_t>(p0 + bw) * ldo + p0 + bw;
+          gemm<true, true>(m2, m2, bw, L21, ldo, L21, ldo, true, sm.gemm, EpiSub{C, ldo});
+        }
+      }
+      // X = K_oo
+      for (int i = warp_id(); i < o; i += NW)
+        for (int j = lane_id(); j < o; j += 32)
+          X[static_cast<int64_t>(i) * ldo + j] = Ke[static_cast<int64_t>(i) * ldk + j];
+      __syncthreads();
+      // forward: L Z = K
+      for (int p0 = 0; p0 < o; p0 += PB) {
+        const int bw = min(PB, o - p0);
+        load_lower_tri(S, ldo, p0, bw, sm.tri);
+        trsm_lower_cols(sm.tri, bw, X, ldo, p0, o);
+        if (p0 + bw < o) {
+          const double *L = S + static_cast<int64_t>(p0 + bw) * ldo + p0;
+          const double *Zp = X + static_cast<int64_t>(p0) * ldo;
+          double *C = X + static_cast<int64_t>(p0 + bw) * ldo;
+          gemm<true, false>(o - p0 - bw, o, bw, L, ldo, Zp, ldo, false, sm.gemm, EpiSub{C, ldo});
+        }
+      }
+      // backward: L^T X = Z
+      for (int p0 = ((o - 1) / PB) * PB; p0 >= 0; p0 -= PB) {
+        const int bw = min(PB, o - p0);
+        load_lower_tri(S, ldo, p0, bw, sm.tri);
+        trsm_lower_t_cols(sm.tri, bw, X, ldo, p0, o);
+        if (p0 > 0) {
+          // X[0:p0] -= (L[p0:p0+bw, 0:p0])^T X[p0:p0+bw]; A(i,k) = S[(p0+k)*ldo + i] -> [K][M]
+          const double *Lt = S + static_cast<int64_t>(p0) * ldo;
+          const double *Xp = X + static_cast<int64_t>(p0) * ldo;
+          gemm<false, false>(p0, o, bw, Lt, ldo, Xp, ldo, false, sm.gemm, EpiSub{X, ldo});
+        }
+      }
+      // P = K_oo X  (into S's storage)
+      gemm<true, false>(o, o, o, Ke, ldk, X, ldo, false, sm.gemm, EpiStore{S, ldo, 0.0});
+    }
+    // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
+    for (int i = warp_id(); i < n; i += NW) {
+      double s = 0.0;
+      for (int j = lane_id(); j < n; j += 32) {
+        double v = 0.0;
+        if (i < o && j < o) {
+          const double x = X[static_cast<int64_t>(i) * ldo + j];
+          const double p = S[static_cast<int64_t>(i) * ldo + j];
+          v = 4.0 * fma(x, x, p * p);
+          if (!isfinite(v)) bad = 1;
+        }
+        if (T2e) T2e[static_cast<int64_t>(i) * n + j] = v;
+        s += v;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (rowsum && lane_id() == 0) rowsum[e * n + i] = s;
+    }
+    bad = __syncthreads_or(bad);
+    if (bad && threadIdx.x == 0) set_status(status, e, RMX_E_NONFINITE);
+  }
+}
+
+int64_t tepi_ws_doubles_per_slot(int64_t nch) {
+  const int64_t npad = (nch + 1) & ~1LL;
+  return 2 * nch * npad;
+}
+
+cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
+                        const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
+                        double *ws, int64_t ws_slots, int32_t *status, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ce = cudaFuncSetAttribute(tepi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sizeof(TepiSmem)));
+    if (ce != cudaSuccess) return ce;
+    attr = true;
+  }
+  const int64_t npad = (nch + 1) & ~1LL;
+  const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
+  tepi_kernel<<<grid, NT, sizeof(TepiSmem), st>>>(K, ldk, kstride, static_cast<int>(nch), ne, n_open,
+                                                  T2, t2_slot, rowsum, ws,
+                                                  tepi_ws_doubles_per_slot(nch),
+                                                  static_cast<int>(npad), status);
+  return cudaGetLastError();
+}
+
+}  // namespace rmx
