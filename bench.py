@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Bench: energies/s of the full R -> K -> |T|^2 sweep (BASELINE.json:2 metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config darc] [--impl reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
+
+A step = one rmx_sweep call (R formation, matching, T epilogue) over one batch of energies of the
+workload's mesh (default: BASELINE.json:10 'darc', nch=2000, nlev=40000, the configuration the
+north_star target is quoted on; it fits one GPU). Energy batches are dealt block-cyclically to the
+ranks (no collective inside the timed region; scaling "weak": fixed energies per GPU per step).
+value  = energies processed by all ranks / max-over-ranks device time (CUDA events, inputs in HBM)
+e2e    = same metric through rmx_sweep_host: host (pinned) inputs -> device -> host row sums
+roofline: dominant kernel = R formation, FP64 DMMA, algorithmic flops nch(nch+1)nlev per energy
+cpu_baseline: the CPU oracle (oracle/) on a bounded sample (rank 0, N = 1 only)
+--impl reference: the oracle itself as the reference arm (PAPER has no runnable reference code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import rmx_synth as syn  # noqa: E402
+from paper_1403_5524_b200 import dist as rdist  # noqa: E402
+
+# FP64 DMMA peak measured on this pool's B200 by tools/fp64_peak.cu (profiles/r01_fp64_peak.jsonl);
+# MEASURED_PEAKS.json carries no FP64 entry and B200_PROFILING.md states no FP64 fallback.
+FP64_DMMA_PEAK_TFLOPS = 37.1
+FP64_DFMA_PEAK_TFLOPS = 34.2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="darc", choices=list(syn.CONFIGS))
+    p.add_argument("--batch", type=int, default=0, help="energies per step (0: library default)")
+    p.add_argument("--impl", default="rmx", choices=["rmx", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--oracle-sample", type=int, default=1, help="energies in the oracle sample")
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, name in enumerate(names):
+                if len(r) > 4 + k and "Active" in r[4 + k] and "Not" not in r[4 + k]:
+                    reasons.add(name)
+        load = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(rows),
+                "reasons": sorted(reasons)}
+
+
+def oracle_baseline(case, idx, threads):
+    """Time the CPU oracle (as it stands) on mesh indices idx; returns (energies/s, seconds)."""
+    import oracle
+    E = case.E[idx]
+    F, G, Fp, Gp = syn.asymptotic(case.eps, E, case.a)
+    no = syn.n_open(case.eps, E)
+    oracle.build()
+    t0 = time.perf_counter()
+    out = oracle.sweep(case.w, case.Ek, case.a, E, F, G, Fp, Gp, no, np.arange(len(idx)),
+                       want=("rowsum",), threads=threads)
+    dt = time.perf_counter() - t0
+    assert np.all(out["status"] == 0)
+    return len(idx) / dt, dt
+
+
+def flops_per_energy(nch, nlev, n_open):
+    no = np.asarray(n_open, dtype=np.float64)
+    fr = nch * (nch + 1.0) * nlev
+    fk = (2.0 / 3.0) * nch ** 3 + 2.0 * nch ** 2 * no
+    ft = (16.0 / 3.0) * no ** 3
+    return fr, fk, ft
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    case = syn.make_case(args.config)
+    threads = os.cpu_count() or 1
+    sample = [case.ne // 2 + s for s in range(max(1, args.oracle_sample))]
+    for _ in range(args.warmup):
+        oracle_baseline(case, sample, threads)
+    times = []
+    for _ in range(args.steps):
+        _, dt = oracle_baseline(case, sample, threads)
+        times.append(dt)
+    tot = sum(times)
+    v = len(sample) * args.steps / tot
+    line = {
+        "impl": "reference", "metric": "energies/sec (R->K->|T|^2 sweep)", "value": v,
+        "unit": "energies/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (oracle: long double)", "data": "synthetic (rmx_synth, seed 0)",
+        "config": {"workload": args.config, **{k: v2 for k, v2 in syn.CONFIGS[args.config].items()}},
+        "cpu_baseline": {"value": v, "unit": "energies/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{len(sample)} energy(ies) at mesh index {sample[0]} of {args.config} per step"},
+        "e2e": {"value": v, "unit": "energies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = rdist.env_rank_world()
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import paper_1403_5524_b200 as rmx
+    torch.cuda.set_device(local)
+    if world > 1:
+        rdist.init_process_group("nccl")
+    dev = torch.device(f"cuda:{local}")
+    cfg = syn.CONFIGS[args.config]
+    nch, nlev = cfg["nch"], cfg["nlev"]
+
+    # ---- inputs: rank 0 generates W/E_k (seeded), broadcast to the other ranks
+    t_setup = time.perf_counter()
+    case = syn.make_case(args.config) if rank == 0 or world == 1 else None
+    ldw = nlev + (nlev & 1)
+    w_d = torch.zeros((nch, ldw), dtype=torch.float64, device=dev)
+    Ek_d = torch.empty(nlev, dtype=torch.float64, device=dev)
+    if case is not None:
+        w_d[:, :nlev] = torch.from_numpy(case.w).to(dev)
+        Ek_d.copy_(torch.from_numpy(case.Ek))
+    if world > 1:
+        rdist.broadcast_inputs([w_d, Ek_d])
+        meta = syn.make_case.__name__  # mesh/thresholds are cheap and seeded: recomputed locally
+        if case is None:
+            case = syn.make_case(args.config)  # thresholds + mesh (W/Ek above come from the broadcast)
+    ctx = rmx.Context(local)
+    ne = case.ne
+    batch = args.batch if args.batch > 0 else 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+    if args.config in ("tiny", "small") and args.batch <= 0:
+        batch = min(ne, 4096 if args.config == "small" else ne)
+    nb = rdist.n_blocks(ne, batch)
+    my_blocks = rdist.cyclic_blocks(ne, batch, world, rank)
+    nsteps = args.warmup + args.steps
+
+    def block_of_step(s):
+        return my_blocks[s % len(my_blocks)]
+
+    step_inputs = []
+    for s in range(nsteps):
+        lo, hi = rdist.block_range(block_of_step(s), ne, batch)
+        E = case.E[lo:hi]
+        F, G, Fp, Gp = syn.asymptotic(case.eps, E, case.a)
+        no = syn.n_open(case.eps, E)
+        step_inputs.append(dict(
+            E=torch.from_numpy(E).to(dev), F=torch.from_numpy(F).to(dev), G=torch.from_numpy(G).to(dev),
+            Fp=torch.from_numpy(Fp).to(dev), Gp=torch.from_numpy(Gp).to(dev),
+            no=torch.from_numpy(no).to(dev), no_host=no, lo=lo, hi=hi))
+    setup_s = time.perf_counter() - t_setup
+
+    def one_step(s):
+        d = step_inputs[s]
+        return ctx.sweep(w_d, Ek_d, case.a, d["E"], d["F"], d["G"], d["Fp"], d["Gp"], d["no"],
+                         batch=batch, prepared=(nlev, ldw))
+
+    # ---- device-resident timed region -------------------------------------------------------
+    for s in range(args.warmup):
+        one_step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ctx.set_timing(True)
+    ctx.reset_stats()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    outs = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for s in range(args.warmup, nsteps):
+            outs.append(one_step(s))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    stats = ctx.stats()
+    ctx.set_timing(False)
+    n_energies_local = sum(step_inputs[s]["hi"] - step_inputs[s]["lo"] for s in range(args.warmup, nsteps))
+    bad = sum(int((o["status"] != 0).sum()) for o in outs)
+    if world > 1:
+        t = torch.tensor([ms, float(n_energies_local)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
+        ms_max, n_energies = float(tmax[0]), int(t[1])
+    else:
+        ms_max, n_energies = ms, n_energies_local
+    value = n_energies / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel (R formation) ---------------------------------------
+    ms_r, n_r = stats["rform"]
+    fr, fk, ft = 0.0, 0.0, 0.0
+    for s in range(args.warmup, nsteps):
+        a, b, c = flops_per_energy(nch, nlev, step_inputs[s]["no_host"])
+        fr += float(np.sum(np.broadcast_to(a, step_inputs[s]["no_host"].shape)))
+        fk += float(np.sum(b))
+        ft += float(np.sum(c))
+    achieved_r = fr / (ms_r / 1e3) / 1e12 if ms_r > 0 else None
+    path_tflops = (fr + fk + ft) / (ms / 1e3) / 1e12
+
+    # ---- results gather (one all-gather, outside the timed region) ---------------------------
+    gather_ms = None
+    if world > 1:
+        loc = torch.cat([o["rowsum"] for o in outs])
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        pad = torch.zeros((args.steps * batch, nch), dtype=torch.float64, device=dev)
+        pad[: loc.shape[0]] = loc
+        full = torch.empty((world * args.steps * batch, nch), dtype=torch.float64, device=dev)
+        torch.distributed.all_gather_into_tensor(full, pad)
+        torch.cuda.synchronize()
+        gather_ms = 1e3 * (time.perf_counter() - g0)
+
+    # ---- end-to-end through the C ABI with host buffers ---------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        w_h = rmx.pinned_empty((nch, ldw))
+        w_h[:] = w_d.cpu().numpy()
+        Ek_h = rmx.pinned_empty((nlev,))
+        Ek_h[:] = Ek_d.cpu().numpy()
+        host_steps = []
+        for s in range(nsteps):
+            d = step_inputs[s]
+            hs = {}
+            for k in ("E", "F", "G", "Fp", "Gp"):
+                a = rmx.pinned_empty(tuple(d[k].shape))
+                a[:] = d[k].cpu().numpy()
+                hs[k] = a
+            a = rmx.pinned_empty(tuple(d["no"].shape), np.int32)
+            a[:] = d["no_host"]
+            hs["no"] = a
+            hs["rowsum"] = rmx.pinned_empty((d["hi"] - d["lo"], nch))
+            hs["status"] = rmx.pinned_empty((d["hi"] - d["lo"],), np.int32)
+            host_steps.append(hs)
+
+        def host_step(s):
+            h = host_steps[s]
+            return ctx.sweep_host(w_h, Ek_h, case.a, h["E"], h["F"], h["G"], h["Fp"], h["Gp"], h["no"],
+                                  batch=batch, rowsum=h["rowsum"], status=h["status"])
+
+        for s in range(args.warmup):
+            host_step(s)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h2d = d2h = 0
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for s in range(args.warmup, nsteps):
+            _, _, hb, db = host_step(s)
+            h2d += hb
+            d2h += db
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": n_energies / (e_ms / 1e3), "unit": "energies/s",
+               "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
+               "includes": "W, E_k, E, F, G, F', G', n_open H2D + rowsum, status D2H every step"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) --------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = [case.ne // 2 + s for s in range(max(1, args.oracle_sample))]
+        if args.config in ("tiny", "small"):
+            sample = list(range(0, case.ne, max(1, case.ne // 256)))
+        threads = os.cpu_count() or 1
+        v, dt = oracle_baseline(case, sample, threads)
+        cpu = {"value": v, "unit": "energies/s", "cores": threads, "kind": "oracle",
+               "sample": f"{len(sample)} energies of {args.config} (mesh index {sample[0]}..{sample[-1]}), "
+                         f"{dt:.1f} s, OpenMP over rows/energies"}
+
+    if rank == 0:
+        line = {
+            "metric": "energies/sec (R->K->|T|^2 sweep)",
+            "value": value, "unit": "energies/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (rmx_synth, seed 0)",
+            "config": {"workload": args.config, "nch": nch, "nlev": nlev, "ne_mesh": ne,
+                       "a": cfg["a"], "energies_per_step_per_gpu": batch,
+                       "parallelism": f"energy-sharded block-cyclic x{world}",
+                       "l2": f"inputs exceed L2 (W = {nch * nlev * 8 / 1e6:.0f} MB, 126 MB L2)"
+                       if nch * nlev * 8 > 126e6 else "W fits L2; R/K batch buffers exceed L2"},
+            "roofline": {"bound": "tensor", "kernel": "rform (FP64 DMMA R formation)",
+                         "achieved": achieved_r, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,
+                         "traffic": None,
+                         "peak_source": "measured FP64 DMMA.8x8x4 peak, tools/fp64_peak.cu on this pool "
+                                        "(profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry",
+                         "algorithmic": "nch(nch+1)*nlev flops per energy x energies per launch"},
+            "kernel_ms": {k: round(v[0], 3) for k, v in stats.items() if k != "launches"},
+            "path_fp64_tflops": path_tflops,
+            "path_fp64_frac": path_tflops / FP64_DMMA_PEAK_TFLOPS,
+            "gpu_launches": int(stats["launches"]),
+            "bad_status_energies": bad,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "setup_s": round(setup_s, 2),
+            "gather_ms": gather_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
