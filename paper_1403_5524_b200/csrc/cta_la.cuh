@@ -20,10 +20,13 @@ constexpr int NW = NT / 32;
 constexpr int BM = 128, BN = 64, BK = 16, WM = 4, WN = 2;
 constexpr int WTM = BM / WM, WTN = BN / WN;  // 32 x 32 warp tile
 constexpr int MI = WTM / 8, NI = WTN / 8;    // 4 x 4 DMMA fragments
-constexpr int PB = 32;                        // panel / block width of the factorizations
+constexpr int PB = 32;                        // inner panel / triangle width of the factorizations
+constexpr int NB = 2 * PB;                    // outer block width (K of the big trailing GEMMs)
 constexpr int A_ELEMS = (BM * (BK + 4) > BK * (BM + 4)) ? BM * (BK + 4) : BK * (BM + 4);
 constexpr int B_ELEMS = (BN * (BK + 4) > BK * (BN + 4)) ? BN * (BK + 4) : BK * (BN + 4);
-constexpr int GEMM_SMEM_DOUBLES = 2 * (A_ELEMS + B_ELEMS);
+constexpr int CS_LD = BN + 8;  // C tile pitch in smem: conflict-free 16-byte fragment reads
+constexpr int C_ELEMS = BM * CS_LD;
+constexpr int GEMM_SMEM_DOUBLES = 2 * (A_ELEMS + B_ELEMS) + C_ELEMS;
 constexpr int TRI_LD = PB + 1;                // padded pitch of a bw x bw triangle in smem
 constexpr int TRI_SMEM_DOUBLES = PB * TRI_LD;
 
@@ -73,17 +76,14 @@ __device__ __forceinline__ void stage_operand(double *s, const double *G, int64_
   }
 }
 
-// Epilogues. acc starts at init2(row, col) for the element pair (col, col+1) and receives A.B;
-// store2 writes the final pair. Element (r, c) is valid iff r < M && c < N (checked by caller
-// through the valid mask v0/v1).
+// Epilogues. kReadC: the accumulator starts from C (staged into shared memory by bulk async
+// copies, one tile ahead of its use); init() maps a C value to the initial accumulator and store2
+// writes the final pair (col, col+1) with the valid masks v0/v1 (r < M && c < N).
 struct EpiSub {  // C -= A.B   (acc = -C ; acc += A.B ; C = -acc : exact sign flips)
+  static constexpr bool kReadC = true;
   double *C;
   int64_t ldc;
-  __device__ __forceinline__ void init2(int r, int c, bool v0, bool v1, double &a0, double &a1) const {
-    const double *p = C + static_cast<int64_t>(r) * ldc + c;
-    a0 = v0 ? -p[0] : 0.0;
-    a1 = v1 ? -p[1] : 0.0;
-  }
+  __device__ __forceinline__ double init(double c) const { return -c; }
   __device__ __forceinline__ void store2(int r, int c, bool v0, bool v1, double a0, double a1) const {
     double *p = C + static_cast<int64_t>(r) * ldc + c;
     if (v0) p[0] = -a0;
@@ -92,19 +92,32 @@ struct EpiSub {  // C -= A.B   (acc = -C ; acc += A.B ; C = -acc : exact sign fl
 };
 
 struct EpiStore {  // C = A.B + diag_add * I
+  static constexpr bool kReadC = false;
   double *C;
   int64_t ldc;
   double diag_add;
-  __device__ __forceinline__ void init2(int, int, bool, bool, double &a0, double &a1) const {
-    a0 = 0.0;
-    a1 = 0.0;
-  }
+  __device__ __forceinline__ double init(double) const { return 0.0; }
   __device__ __forceinline__ void store2(int r, int c, bool v0, bool v1, double a0, double a1) const {
     double *p = C + static_cast<int64_t>(r) * ldc + c;
     if (v0) p[0] = a0 + (r == c ? diag_add : 0.0);
     if (v1) p[1] = a1 + (r == c + 1 ? diag_add : 0.0);
   }
 };
+
+// Per-kernel shared state of the C-tile bulk-copy pipeline (one mbarrier, phase carried across calls).
+struct GemmSync {
+  uint64_t cbar;
+  uint32_t cphase;
+  uint32_t pad;
+};
+__device__ __forceinline__ void gemm_sync_init(GemmSync *gs) {
+  if (threadIdx.x == 0) {
+    mbar_init(&gs->cbar, 1);
+    gs->cphase = 0;
+    fence_barrier_init();
+  }
+  __syncthreads();
+}
 
 // Tile enumeration (row-major over tm); lower = only tiles holding some element with row >= col.
 __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
@@ -113,11 +126,30 @@ __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
   return min(tiles_n, last_col_tile + 1);
 }
 
-// C[M x N] op= A[M x K] . B[K x N]. smem: GEMM_SMEM_DOUBLES doubles. Must be called by all
-// threads; begins and ends with a __syncthreads().
+// Warp 0: bulk-copy the valid rows of C tile (tm, tn) into Cs (pitch CS_LD), completion on cbar.
+// Rows are copied as whole 16-byte chunks (may read <= 8 bytes past the last column: workspaces are
+// padded for this).
+__device__ __forceinline__ void issue_c_tile(const double *C, int64_t ldc, int M, int N, int tm,
+                                             int tn, double *Cs, uint64_t *cbar) {
+  const int lane = lane_id();
+  const int r0 = tm * BM, c0 = tn * BN;
+  const int rows = min(BM, M - r0), cols = min(BN, N - c0);
+  const uint32_t rb = static_cast<uint32_t>((cols * 8 + 15) & ~15);
+  if (lane == 0) mbar_arrive_expect_tx(cbar, rb * static_cast<uint32_t>(rows));
+  __syncwarp();
+  for (int r = lane; r < rows; r += 32)
+    bulk_g2s(smem_u32(Cs + r * CS_LD), C + static_cast<int64_t>(r0 + r) * ldc + c0, rb, cbar);
+}
+
+// C[M x N] op= A[M x K] . B[K x N] on the calling CTA. smem: GEMM_SMEM_DOUBLES doubles (A/B
+// double buffer for cp.async, plus the C tile buffer). Begins and ends with __syncthreads().
+// Pipeline: A/B k-slices (BK) double-buffered with cp.async groups; the next tile's C is fetched by
+// cp.async.bulk into Cs as soon as the current tile's accumulators have been initialised from it,
+// so its latency overlaps a whole tile of DMMA work.
 template <bool A_KC, bool B_KC, class Epi>
 __device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t lda, const double *B,
-                     int64_t ldb, bool lower, double *smem, const Epi &epi) {
+                                  int64_t ldb, bool lower, double *smem, GemmSync *gs,
+                                  const Epi &epi) {
   __syncthreads();
   if (M <= 0 || N <= 0) return;
   const int tiles_m = cdiv(M, BM), tiles_n = cdiv(N, BN);
@@ -127,16 +159,19 @@ __device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t 
   const int total = ntiles * nkc;
   const bool al16 = ((lda | ldb) & 1) == 0 &&
                     ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+  bool bulk_c = false;
+  if constexpr (Epi::kReadC)
+    bulk_c = (epi.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(epi.C) & 15) == 0;
   double *As[2] = {smem, smem + A_ELEMS};
   double *Bs[2] = {smem + 2 * A_ELEMS, smem + 2 * A_ELEMS + B_ELEMS};
+  double *Cs = smem + 2 * (A_ELEMS + B_ELEMS);
+  uint32_t ph = gs->cphase;
 
   const int warp = warp_id(), lane = lane_id();
   const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, t = lane & 3;
 
-  auto decode = [&](int it, int &tm, int &tn, int &kc) {
-    int tile = it / nkc;
-    kc = it % nkc;
+  auto decode_tile = [&](int tile, int &tm, int &tn) {
     tm = 0;
     int cnt;
     while (tile >= (cnt = tiles_in_row(tm, tiles_n, lower))) {
@@ -145,29 +180,53 @@ __device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t 
     }
     tn = tile;
   };
-  auto issue = [&](int it) {
-    int tm, tn, kc;
-    decode(it, tm, tn, kc);
-    const int buf = it & 1;
+  auto issue_ab = [&](int it) {
+    int tm, tn;
+    decode_tile(it / nkc, tm, tn);
+    const int kc = it % nkc, buf = it & 1;
     stage_operand<A_KC, BM>(As[buf], A, lda, tm * BM, kc * BK, M, K, al16);
     stage_operand<B_KC, BN>(Bs[buf], B, ldb, tn * BN, kc * BK, N, K, al16);
     cp_async_commit();
   };
 
+  if (bulk_c && warp == 0) {
+    int tm, tn;
+    decode_tile(0, tm, tn);
+    issue_c_tile(epi.C, epi.ldc, M, N, tm, tn, Cs, &gs->cbar);
+  }
+  issue_ab(0);
   double acc[MI][NI][2];
-  issue(0);
   for (int it = 0; it < total; ++it) {
-    int tm, tn, kc;
-    decode(it, tm, tn, kc);
-    if (it + 1 < total) issue(it + 1);
+    const int tile = it / nkc, kc = it % nkc;
+    int tm, tn;
+    decode_tile(tile, tm, tn);
+    if (it + 1 < total) issue_ab(it + 1);
     if (kc == 0) {
+      if (bulk_c) {
+        mbar_wait(&gs->cbar, ph);
+        ph ^= 1;
+      }
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) {
-        const int r = tm * BM + wm * WTM + mi * 8 + g;
+        const int rl = wm * WTM + mi * 8 + g;
+        const int r = tm * BM + rl;
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) {
-          const int c = tn * BN + wn * WTN + ni * 8 + 2 * t;
-          epi.init2(r, c, r < M && c < N, r < M && c + 1 < N, acc[mi][ni][0], acc[mi][ni][1]);
+          const int cl = wn * WTN + ni * 8 + 2 * t;
+          const int c = tn * BN + cl;
+          double c0v = 0.0, c1v = 0.0;
+          if constexpr (Epi::kReadC) {
+            if (bulk_c) {
+              c0v = Cs[rl * CS_LD + cl];
+              c1v = Cs[rl * CS_LD + cl + 1];
+            } else {
+              const double *p = epi.C + static_cast<int64_t>(r) * epi.ldc + c;
+              if (r < M && c < N) c0v = p[0];
+              if (r < M && c + 1 < N) c1v = p[1];
+            }
+          }
+          acc[mi][ni][0] = epi.init(c0v);
+          acc[mi][ni][1] = epi.init(c1v);
         }
       }
     }
@@ -176,6 +235,12 @@ __device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t 
     else
       cp_async_wait<0>();
     __syncthreads();
+    if (kc == 0 && bulk_c && tile + 1 < ntiles && warp == 0) {
+      int tm2, tn2;
+      decode_tile(tile + 1, tm2, tn2);
+      fence_proxy_async();
+      issue_c_tile(epi.C, epi.ldc, M, N, tm2, tn2, Cs, &gs->cbar);
+    }
     if (K > 0) {
       const double *as = As[it & 1], *bs = Bs[it & 1];
 #pragma unroll
@@ -212,6 +277,7 @@ __device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t 
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) gs->cphase = ph;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -245,14 +311,16 @@ __device__ __forceinline__ void block_argmax(double &v, int &idx, double *redv, 
 }
 
 // LU with partial pivoting of the panel M[p0:n, p0:p0+bw] (bw <= 32), in place: multipliers
-// below the diagonal, U on and above. Row swaps are applied inside the panel only; the pivot
-// rows are returned in ipiv[0..bw) (absolute row indices). Returns 1 on an exact zero pivot.
-// The rank-1 update of column j is fused with the pivot search of column j+1 (one pass per column).
-static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0, int bw, int *ipiv, double *redv,
-                        int *redi) {
+// below the diagonal, U on and above. Each interchange swaps the two rows over the columns
+// [sc0, sc1) (the whole augmented row right of the current outer block, so the trailing matrix,
+// the right-hand sides and the outer block's earlier multipliers stay consistent); the pivot rows
+// are also recorded in ipiv[0..bw). Returns 1 on an exact zero pivot. The rank-1 update of column
+// j is fused with the pivot search of column j+1 (one pass over the rows per column).
+// Pivot rule: max |a_ij|, ties -> lowest row (the oracle's rule).
+static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0, int bw, int sc0,
+                                            int sc1, int *ipiv, double *redv, int *redi) {
   const int warp = warp_id(), lane = lane_id();
   int singular = 0;
-  // pivot search for the first column
   double best = -1.0;
   int besti = n;
   for (int i = p0 + threadIdx.x; i < n; i += NT) {
@@ -266,12 +334,29 @@ static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0
   for (int jj = 0; jj < bw; ++jj) {
     const int j = p0 + jj;
     const int pr = besti < n ? besti : j;  // all-NaN column (e.g. a pole energy): no interchange
-    if (pr != j && warp == 0 && lane < bw) {
-      double *a = M + static_cast<int64_t>(j) * ld + p0 + lane;
-      double *b = M + static_cast<int64_t>(pr) * ld + p0 + lane;
-      const double tmp = *a;
-      *a = *b;
-      *b = tmp;
+    if (pr != j) {
+      double *a = M + static_cast<int64_t>(j) * ld;
+      double *b = M + static_cast<int64_t>(pr) * ld;
+      constexpr int SU = 4;
+      for (int c0 = sc0 + threadIdx.x; c0 < sc1; c0 += NT * SU) {
+        double va[SU], vb[SU];
+#pragma unroll
+        for (int q = 0; q < SU; ++q) {
+          const int c = c0 + q * NT;
+          if (c < sc1) {
+            va[q] = a[c];
+            vb[q] = b[c];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < SU; ++q) {
+          const int c = c0 + q * NT;
+          if (c < sc1) {
+            a[c] = vb[q];
+            b[c] = va[q];
+          }
+        }
+      }
     }
     if (threadIdx.x == 0) ipiv[jj] = pr;
     __syncthreads();
@@ -279,11 +364,12 @@ static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0
     const double piv = __shfl_sync(0xffffffffu, u, jj);
     const bool zero = (piv == 0.0);
     singular |= zero;
+    const double rpiv = zero ? 0.0 : 1.0 / piv;
     best = -1.0;
     besti = n;
     const bool track = (jj + 1 < bw);
-    // rows j+1 .. n-1, warp-strided, 4 rows in flight per warp
-    constexpr int UNR = 4;
+    // rows j+1 .. n-1, warp-strided, UNR rows in flight per warp
+    constexpr int UNR = 8;
     for (int i0 = j + 1 + warp; i0 < n; i0 += NW * UNR) {
       double x[UNR];
 #pragma unroll
@@ -295,7 +381,7 @@ static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0
       for (int q = 0; q < UNR; ++q) {
         const int i = i0 + q * NW;
         const double xj = __shfl_sync(0xffffffffu, x[q], jj);
-        const double l = zero ? 0.0 : xj / piv;
+        const double l = xj * rpiv;
         double y = x[q];
         if (lane == jj)
           y = zero ? xj : l;
@@ -317,26 +403,16 @@ static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0
   return singular;
 }
 
-// Apply the panel's row interchanges to columns [c0, c1) and solve U12 = L11^{-1} A12 for the
-// panel rows (L11 unit lower from M[p0:p0+bw, p0:p0+bw]). One thread per column.
-static __device__ __noinline__ void swap_and_trsm_unit_lower(double *M, int64_t ld, int p0, int bw, const int *ipiv,
-                                         int c0, int c1, double *tri) {
-  for (int q = threadIdx.x; q < bw * bw; q += NT) {
-    const int r = q / bw, c = q % bw;
-    tri[r * TRI_LD + c] = M[static_cast<int64_t>(p0 + r) * ld + p0 + c];
+// U12 = L11^{-1} A12 for the rows [p0, p0+bw) and columns [c0, c1), L11 = unit lower part of
+// M[p0:p0+bw, p0:p0+bw] (bw <= 32). One thread per column.
+static __device__ __noinline__ void trsm_unit_lower_cols(double *M, int64_t ld, int p0, int bw,
+                                                         int c0, int c1, double *tri) {
+  for (int q = threadIdx.x; q < PB * PB; q += NT) {
+    const int r = q / PB, c = q % PB;
+    tri[r * TRI_LD + c] = (r < bw && c < r) ? M[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
   }
   __syncthreads();
   for (int c = c0 + threadIdx.x; c < c1; c += NT) {
-    for (int jj = 0; jj < bw; ++jj) {
-      const int pr = ipiv[jj];
-      if (pr != p0 + jj) {
-        double *a = M + static_cast<int64_t>(p0 + jj) * ld + c;
-        double *b = M + static_cast<int64_t>(pr) * ld + c;
-        const double tmp = *a;
-        *a = *b;
-        *b = tmp;
-      }
-    }
     double x[PB];
 #pragma unroll
     for (int r = 0; r < PB; ++r) x[r] = r < bw ? M[static_cast<int64_t>(p0 + r) * ld + c] : 0.0;

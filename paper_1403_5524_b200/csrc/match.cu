@@ -16,12 +16,18 @@ struct MatchSmem {
   double tri[TRI_SMEM_DOUBLES];
   double redv[NW];
   int redi[NW];
-  int ipiv[PB];
+  int ipiv[NB];
+  GemmSync gs;
 };
 
 // Workspace slot M [n][ldm] = [A | pad | B_open]; after elimination + back substitution the
 // columns [npad, npad + o) hold Y = A^{-1} B_open and K[e] = -Y (open), -e_j (closed).
 // K may alias R (the sweep reuses the R batch buffer): R[e] is fully consumed before K[e] is written.
+//
+// LU: outer blocks of NB = 64 columns, each factored as two inner panels of PB = 32 (the second
+// after a K = 32 update of the block's right half), so that the big trailing updates run with
+// K = 64 (half the C-tile traffic per flop of K = 32). Interchanges swap whole augmented rows right
+// of the outer block's start (LAPACK getrf semantics restricted to what the solve needs).
 __global__ void __launch_bounds__(NT, 1)
     match_kernel(const double *R, int64_t ldr, const double *__restrict__ F,
                  const double *__restrict__ G, const double *__restrict__ Fp,
@@ -30,8 +36,10 @@ __global__ void __launch_bounds__(NT, 1)
                  int64_t ws_slot, int ldm, int32_t *status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   MatchSmem &sm = *reinterpret_cast<MatchSmem *>(smem_raw);
+  gemm_sync_init(&sm.gs);
   double *Mw = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
   const int npad = (n + 1) & ~1;
+  auto Mp = [&](int r, int c) { return Mw + static_cast<int64_t>(r) * ldm + c; };
 
   for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
     int o = n_open ? n_open[e] : n;
@@ -40,51 +48,81 @@ __global__ void __launch_bounds__(NT, 1)
     const double *Re = R + e * static_cast<int64_t>(n) * ldr;
     const double *Fe = F + e * n, *Ge = G + e * n, *Fpe = Fp + e * n, *Gpe = Gp + e * n;
 
-    // ---- S3: A_ij = G_i d_ij - a R_ij G'_j ; B_ij = F_i d_ij - a R_ij F'_j ----
+    // ---- S3: A_ij = G_i d_ij - a R_ij G'_j ; B_ij = F_i d_ij - a R_ij F'_j (4 loads in flight) ----
     for (int i = warp_id(); i < n; i += NW) {
       const double *Ri = Re + static_cast<int64_t>(i) * ldr;
       double *Mi = Mw + static_cast<int64_t>(i) * ldm;
-      for (int j = lane_id(); j < ncols; j += 32) {
-        double v = 0.0;
-        if (j < n) {
-          v = -(a * Ri[j]) * Gpe[j];
-          if (j == i) v += Ge[i];
-        } else if (j >= npad) {
-          const int jb = j - npad;
-          v = -(a * Ri[jb]) * Fpe[jb];
-          if (jb == i) v += Fe[i];
+      constexpr int U = 4;
+      for (int j0 = lane_id(); j0 < ncols; j0 += 32 * U) {
+        double rv[U], sv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int j = j0 + 32 * q;
+          rv[q] = 0.0;
+          sv[q] = 0.0;
+          if (j < n) {
+            rv[q] = Ri[j];
+            sv[q] = Gpe[j];
+          } else if (j >= npad && j < ncols) {
+            rv[q] = Ri[j - npad];
+            sv[q] = Fpe[j - npad];
+          }
         }
-        Mi[j] = v;
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int j = j0 + 32 * q;
+          if (j < ncols) {
+            double v = -(a * rv[q]) * sv[q];
+            if (j == i) v += Ge[i];
+            if (j - npad == i) v += Fe[i];
+            Mi[j] = v;
+          }
+        }
       }
     }
     __syncthreads();
 
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
     int singular = 0;
-    for (int p0 = 0; p0 < n; p0 += PB) {
-      const int bw = min(PB, n - p0);
-      singular |= panel_lu(Mw, ldm, n, p0, bw, sm.ipiv, sm.redv, sm.redi);
-      swap_and_trsm_unit_lower(Mw, ldm, p0, bw, sm.ipiv, p0 + bw, ncols, sm.tri);
-      const int m2 = n - p0 - bw, n2 = ncols - p0 - bw;
-      if (m2 > 0 && n2 > 0) {
-        double *C = Mw + static_cast<int64_t>(p0 + bw) * ldm + p0 + bw;
-        const double *L21 = Mw + static_cast<int64_t>(p0 + bw) * ldm + p0;
-        const double *U12 = Mw + static_cast<int64_t>(p0) * ldm + p0 + bw;
-        gemm<true, false>(m2, n2, bw, L21, ldm, U12, ldm, false, sm.gemm, EpiSub{C, ldm});
+    for (int P0 = 0; P0 < n; P0 += NB) {
+      const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
+      singular |= panel_lu(Mw, ldm, n, P0, w1, P0, ncols, sm.ipiv, sm.redv, sm.redi);
+      if (w2 > 0) {
+        // right half of the outer block: U_ab = L_aa^{-1} A_ab, then A_bb.. -= L_.a U_ab
+        trsm_unit_lower_cols(Mw, ldm, P0, w1, P0 + w1, P0 + W, sm.tri);
+        gemm<true, false>(n - P0 - w1, w2, w1, Mp(P0 + w1, P0), ldm, Mp(P0, P0 + w1), ldm, false,
+                          sm.gemm, &sm.gs, EpiSub{Mp(P0 + w1, P0 + w1), ldm});
+        singular |= panel_lu(Mw, ldm, n, P0 + w1, w2, P0, ncols, sm.ipiv + PB, sm.redv, sm.redi);
+      }
+      if (P0 + W < ncols) {
+        // U12 = L11^{-1} A12 over the trailing columns, L11 = [[L_aa, 0], [L_ba, L_bb]]
+        trsm_unit_lower_cols(Mw, ldm, P0, w1, P0 + W, ncols, sm.tri);
+        if (w2 > 0) {
+          gemm<true, false>(w2, ncols - P0 - W, w1, Mp(P0 + w1, P0), ldm, Mp(P0, P0 + W), ldm, false,
+                            sm.gemm, &sm.gs, EpiSub{Mp(P0 + w1, P0 + W), ldm});
+          trsm_unit_lower_cols(Mw, ldm, P0 + w1, w2, P0 + W, ncols, sm.tri);
+        }
+        // trailing update with K = W
+        if (P0 + W < n)
+          gemm<true, false>(n - P0 - W, ncols - P0 - W, W, Mp(P0 + W, P0), ldm, Mp(P0, P0 + W), ldm,
+                            false, sm.gemm, &sm.gs, EpiSub{Mp(P0 + W, P0 + W), ldm});
       }
     }
 
     // ---- S4b: blocked back substitution U Y = L^{-1} P B_open (Y in columns [npad, npad+o)) ----
     if (o > 0) {
       double *Y = Mw + npad;
-      for (int p0 = ((n - 1) / PB) * PB; p0 >= 0; p0 -= PB) {
-        const int bw = min(PB, n - p0);
-        trsm_upper_cols(Mw, ldm, p0, bw, Y, ldm, o, sm.tri);
-        if (p0 > 0) {
-          const double *U = Mw + p0;  // rows [0, p0), cols [p0, p0+bw): A[i][k] = U[i*ldm + k]
-          const double *Yp = Y + static_cast<int64_t>(p0) * ldm;
-          gemm<true, false>(p0, o, bw, U, ldm, Yp, ldm, false, sm.gemm, EpiSub{Y, ldm});
+      for (int P0 = ((n - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
+        const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
+        if (w2 > 0) {
+          trsm_upper_cols(Mw, ldm, P0 + w1, w2, Y, ldm, o, sm.tri);
+          gemm<true, false>(w1, o, w2, Mp(P0, P0 + w1), ldm, Y + static_cast<int64_t>(P0 + w1) * ldm,
+                            ldm, false, sm.gemm, &sm.gs, EpiSub{Y + static_cast<int64_t>(P0) * ldm, ldm});
         }
+        trsm_upper_cols(Mw, ldm, P0, w1, Y, ldm, o, sm.tri);
+        if (P0 > 0)
+          gemm<true, false>(P0, o, W, Mp(0, P0), ldm, Y + static_cast<int64_t>(P0) * ldm, ldm, false,
+                            sm.gemm, &sm.gs, EpiSub{Y, ldm});
       }
     }
 
@@ -119,7 +157,7 @@ size_t match_smem_bytes() { return sizeof(MatchSmem); }
 
 int64_t match_ws_doubles_per_slot(int64_t nch) {
   const int64_t npad = (nch + 1) & ~1LL;
-  return nch * (2 * npad);
+  return nch * (2 * npad) + 32;  // + tail padding for 16-byte bulk copies of odd-width C tiles
 }
 
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,

@@ -16,16 +16,22 @@ using namespace la;
 struct TepiSmem {
   double gemm[GEMM_SMEM_DOUBLES];
   double tri[TRI_SMEM_DOUBLES];
+  GemmSync gs;
 };
 
+// Factorisation / solves use outer blocks of NB = 64 (two inner 32-wide triangles) so that the
+// big updates run with K = 64.
 __global__ void __launch_bounds__(NT, 1)
     tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
                 const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
                 double *rowsum, double *ws, int64_t ws_slot, int ldo, int32_t *status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TepiSmem &sm = *reinterpret_cast<TepiSmem *>(smem_raw);
+  gemm_sync_init(&sm.gs);
   double *S = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;  // o x ldo; later holds P
   double *X = S + static_cast<int64_t>(n) * ldo;                // o x ldo
+  auto Sp = [&](int r, int c) { return S + static_cast<int64_t>(r) * ldo + c; };
+  auto Xr = [&](int r) { return X + static_cast<int64_t>(r) * ldo; };
 
   for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
     int o = n_open ? n_open[e] : n;
@@ -39,50 +45,62 @@ __global__ void __launch_bounds__(NT, 1)
     int bad = 0;
     if (o > 0) {
       // S = I + K_oo K_oo^T (lower tiles)
-      gemm<true, true>(o, o, o, Ke, ldk, Ke, ldk, true, sm.gemm, EpiStore{S, ldo, 1.0});
-      // blocked Cholesky, lower
-      for (int p0 = 0; p0 < o; p0 += PB) {
-        const int bw = min(PB, o - p0);
-        bad |= chol_diag(S, ldo, p0, bw, sm.tri);
-        if (p0 + bw < o) {
-          trsm_rows_lt(sm.tri, bw, S, ldo, p0, p0 + bw, o);
-          const int m2 = o - p0 - bw;
-          const double *L21 = S + static_cast<int64_t>(p0 + bw) * ldo + p0;
-          double *C = S + static_cast<int64_t>(p0 + bw) * ldo + p0 + bw;
-          gemm<true, true>(m2, m2, bw, L21, ldo, L21, ldo, true, sm.gemm, EpiSub{C, ldo});
+      gemm<true, true>(o, o, o, Ke, ldk, Ke, ldk, true, sm.gemm, &sm.gs, EpiStore{S, ldo, 1.0});
+      // blocked Cholesky S = L L^T (lower)
+      for (int P0 = 0; P0 < o; P0 += NB) {
+        const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
+        bad |= chol_diag(S, ldo, P0, w1, sm.tri);
+        if (P0 + w1 < o) trsm_rows_lt(sm.tri, w1, S, ldo, P0, P0 + w1, o);
+        if (w2 > 0) {
+          gemm<true, true>(o - P0 - w1, w2, w1, Sp(P0 + w1, P0), ldo, Sp(P0 + w1, P0), ldo, false,
+                           sm.gemm, &sm.gs, EpiSub{Sp(P0 + w1, P0 + w1), ldo});
+          bad |= chol_diag(S, ldo, P0 + w1, w2, sm.tri);
+          if (P0 + W < o) trsm_rows_lt(sm.tri, w2, S, ldo, P0 + w1, P0 + W, o);
+        }
+        if (P0 + W < o) {
+          const int m2 = o - P0 - W;
+          gemm<true, true>(m2, m2, W, Sp(P0 + W, P0), ldo, Sp(P0 + W, P0), ldo, true, sm.gemm, &sm.gs,
+                           EpiSub{Sp(P0 + W, P0 + W), ldo});
         }
       }
       // X = K_oo
       for (int i = warp_id(); i < o; i += NW)
-        for (int j = lane_id(); j < o; j += 32)
-          X[static_cast<int64_t>(i) * ldo + j] = Ke[static_cast<int64_t>(i) * ldk + j];
+        for (int j = lane_id(); j < o; j += 32) Xr(i)[j] = Ke[static_cast<int64_t>(i) * ldk + j];
       __syncthreads();
       // forward: L Z = K
-      for (int p0 = 0; p0 < o; p0 += PB) {
-        const int bw = min(PB, o - p0);
-        load_lower_tri(S, ldo, p0, bw, sm.tri);
-        trsm_lower_cols(sm.tri, bw, X, ldo, p0, o);
-        if (p0 + bw < o) {
-          const double *L = S + static_cast<int64_t>(p0 + bw) * ldo + p0;
-          const double *Zp = X + static_cast<int64_t>(p0) * ldo;
-          double *C = X + static_cast<int64_t>(p0 + bw) * ldo;
-          gemm<true, false>(o - p0 - bw, o, bw, L, ldo, Zp, ldo, false, sm.gemm, EpiSub{C, ldo});
+      for (int P0 = 0; P0 < o; P0 += NB) {
+        const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
+        load_lower_tri(S, ldo, P0, w1, sm.tri);
+        trsm_lower_cols(sm.tri, w1, X, ldo, P0, o);
+        if (w2 > 0) {
+          gemm<true, false>(w2, o, w1, Sp(P0 + w1, P0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
+                            EpiSub{Xr(P0 + w1), ldo});
+          load_lower_tri(S, ldo, P0 + w1, w2, sm.tri);
+          trsm_lower_cols(sm.tri, w2, X, ldo, P0 + w1, o);
         }
+        if (P0 + W < o)
+          gemm<true, false>(o - P0 - W, o, W, Sp(P0 + W, P0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
+                            EpiSub{Xr(P0 + W), ldo});
       }
       // backward: L^T X = Z
-      for (int p0 = ((o - 1) / PB) * PB; p0 >= 0; p0 -= PB) {
-        const int bw = min(PB, o - p0);
-        load_lower_tri(S, ldo, p0, bw, sm.tri);
-        trsm_lower_t_cols(sm.tri, bw, X, ldo, p0, o);
-        if (p0 > 0) {
-          // X[0:p0] -= (L[p0:p0+bw, 0:p0])^T X[p0:p0+bw]; A(i,k) = S[(p0+k)*ldo + i] -> [K][M]
-          const double *Lt = S + static_cast<int64_t>(p0) * ldo;
-          const double *Xp = X + static_cast<int64_t>(p0) * ldo;
-          gemm<false, false>(p0, o, bw, Lt, ldo, Xp, ldo, false, sm.gemm, EpiSub{X, ldo});
+      for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
+        const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
+        if (w2 > 0) {
+          load_lower_tri(S, ldo, P0 + w1, w2, sm.tri);
+          trsm_lower_t_cols(sm.tri, w2, X, ldo, P0 + w1, o);
+          // X[P0:P0+w1] -= (L[P0+w1:P0+W, P0:P0+w1])^T X[P0+w1:P0+W]; A(i,k) = S[(P0+w1+k), P0+i]
+          gemm<false, false>(w1, o, w2, Sp(P0 + w1, P0), ldo, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
+                             EpiSub{Xr(P0), ldo});
         }
+        load_lower_tri(S, ldo, P0, w1, sm.tri);
+        trsm_lower_t_cols(sm.tri, w1, X, ldo, P0, o);
+        if (P0 > 0)
+          // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]; A(i,k) = S[(P0+k)*ldo + i] -> [K][M]
+          gemm<false, false>(P0, o, W, Sp(P0, 0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
+                             EpiSub{X, ldo});
       }
       // P = K_oo X  (into S's storage)
-      gemm<true, false>(o, o, o, Ke, ldk, X, ldo, false, sm.gemm, EpiStore{S, ldo, 0.0});
+      gemm<true, false>(o, o, o, Ke, ldk, X, ldo, false, sm.gemm, &sm.gs, EpiStore{S, ldo, 0.0});
     }
     // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
@@ -90,8 +108,8 @@ __global__ void __launch_bounds__(NT, 1)
       for (int j = lane_id(); j < n; j += 32) {
         double v = 0.0;
         if (i < o && j < o) {
-          const double x = X[static_cast<int64_t>(i) * ldo + j];
-          const double p = S[static_cast<int64_t>(i) * ldo + j];
+          const double x = Xr(i)[j];
+          const double p = *Sp(i, j);
           v = 4.0 * fma(x, x, p * p);
           if (!isfinite(v)) bad = 1;
         }
@@ -109,7 +127,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 int64_t tepi_ws_doubles_per_slot(int64_t nch) {
   const int64_t npad = (nch + 1) & ~1LL;
-  return 2 * nch * npad;
+  return 2 * nch * npad + 32;  // + tail padding for 16-byte bulk copies of odd-width C tiles
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
