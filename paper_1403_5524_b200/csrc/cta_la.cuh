@@ -3,11 +3,13 @@
 // threads of one CTA; there is no inter-CTA communication (one CTA owns one energy, SURVEY.md
 // §8(a) S4/S5 and BASELINE.json:5 "one CTA ... per energy").
 //
-//   gemm      : C op= A.B over a tile loop, 128x64 CTA tiles, FP64 DMMA (mma.m8n8k4.f64) with a
-//               2-stage cp.async pipeline; A stored [M][K] or [K][M], B stored [N][K] or [K][N]
+//   gemm      : C op= A.B over a tile loop, 128x64 CTA tiles, FP64 DMMA (mma.m8n8k4.f64) fed by a
+//               warp-specialised cp.async.bulk + mbarrier pipeline; A stored [M][K] or [K][M],
+//               B stored [N][K] or [K][N]; C read (C -= A.B) or written (C = A.B)
 //   panel_lu  : unblocked LU with partial pivoting of an n x bw panel (pivot = max |a|, ties ->
 //               lowest row, the oracle's rule), rank-1 updates fused with the next pivot search
-//   trsm_*    : small (bw <= 32) triangular solves, one thread per column / row
+//   tri_inv   : inverse of a 32 x 32 triangular diagonal block; all triangular solves are then
+//               DMMA GEMMs with it (in place)
 //   chol_diag : unblocked Cholesky of a bw x bw diagonal block in shared memory
 #pragma once
 #include "rmx_common.cuh"
@@ -15,66 +17,29 @@
 namespace rmx {
 namespace la {
 
-constexpr int NT = 256;  // threads per CTA
+constexpr int NT = 288;  // threads per CTA: 8 DMMA consumer warps + 1 copy-producer warp
 constexpr int NW = NT / 32;
-constexpr int BM = 128, BN = 64, BK = 16, WM = 4, WN = 2;
+constexpr int NCW = 8;          // consumer warps inside gemm(); warp NCW is the producer
+constexpr int BM = 128, BN = 64, BK = 32, WM = 4, WN = 2;
 constexpr int WTM = BM / WM, WTN = BN / WN;  // 32 x 32 warp tile
 constexpr int MI = WTM / 8, NI = WTN / 8;    // 4 x 4 DMMA fragments
 constexpr int PB = 32;                        // inner panel / triangle width of the factorizations
 constexpr int NB = 2 * PB;                    // outer block width (K of the big trailing GEMMs)
-constexpr int A_ELEMS = (BM * (BK + 4) > BK * (BM + 4)) ? BM * (BK + 4) : BK * (BM + 4);
-constexpr int B_ELEMS = (BN * (BK + 4) > BK * (BN + 4)) ? BN * (BK + 4) : BK * (BN + 4);
+constexpr int STAGES = 2;                     // A/B ring depth
+// smem pitches (doubles), chosen for conflict-free fragment loads:
+//   k-contiguous tiles [rows][KC_LD]   : 16-byte LDS of (k, k+1), row stride = 64 mod 128 bytes
+//   m/n-contiguous tiles [k][X_LD]     : 8-byte LDS, 4*ld = 8 mod 32 banks
+constexpr int KC_LD = BK + 8;
+constexpr int A_MC_LD = BM + 2, B_NC_LD = BN + 2;
+constexpr int A_ELEMS = (BM * KC_LD > BK * A_MC_LD) ? BM * KC_LD : BK * A_MC_LD;
+constexpr int B_ELEMS = (BN * KC_LD > BK * B_NC_LD) ? BN * KC_LD : BK * B_NC_LD;
 constexpr int CS_LD = BN + 8;  // C tile pitch in smem: conflict-free 16-byte fragment reads
 constexpr int C_ELEMS = BM * CS_LD;
-constexpr int GEMM_SMEM_DOUBLES = 2 * (A_ELEMS + B_ELEMS) + C_ELEMS;
+constexpr int GEMM_SMEM_DOUBLES = STAGES * (A_ELEMS + B_ELEMS) + C_ELEMS;
 constexpr int TRI_LD = PB + 1;                // padded pitch of a bw x bw triangle in smem
 constexpr int TRI_SMEM_DOUBLES = PB * TRI_LD;
 
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
-
-// ------------------------------------------------------------------------------------------------
-// cp.async staging of one BK-slice of an operand tile
-//   KC  : global element (r, k) at G[r*ld + k]  -> smem [ROWS][BK+4]
-//   !KC : global element (r, k) at G[k*ld + r]  -> smem [BK][ROWS+4]
-// rows >= R or k >= K are zero-filled. al16: ld even and G 16-byte aligned.
-template <bool KC, int ROWS>
-__device__ __forceinline__ void stage_operand(double *s, const double *G, int64_t ld, int r0,
-                                              int k0, int R, int K, bool al16) {
-  const uint32_t sb = smem_u32(s);
-  if (KC) {
-    constexpr int CPR = BK / 2;  // 16-byte chunks per row
-    for (int q = threadIdx.x; q < ROWS * CPR; q += NT) {
-      const int r = q / CPR, kc = (q % CPR) * 2;
-      const int gr = r0 + r, gk = k0 + kc;
-      int nv = (gr < R) ? K - gk : 0;
-      nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
-      const double *src = nv ? G + static_cast<int64_t>(gr) * ld + gk : G;
-      const uint32_t dst = sb + (r * (BK + 4) + kc) * 8;
-      if (al16) {
-        cp_async16(dst, src, nv * 8);
-      } else {
-        cp_async8(dst, src, nv > 0 ? 8 : 0);
-        cp_async8(dst + 8, nv > 1 ? src + 1 : G, nv > 1 ? 8 : 0);
-      }
-    }
-  } else {
-    constexpr int CPR = ROWS / 2;
-    for (int q = threadIdx.x; q < BK * CPR; q += NT) {
-      const int kk = q / CPR, rc = (q % CPR) * 2;
-      const int gk = k0 + kk, gr = r0 + rc;
-      int nv = (gk < K) ? R - gr : 0;
-      nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
-      const double *src = nv ? G + static_cast<int64_t>(gk) * ld + gr : G;
-      const uint32_t dst = sb + (kk * (ROWS + 4) + rc) * 8;
-      if (al16) {
-        cp_async16(dst, src, nv * 8);
-      } else {
-        cp_async8(dst, src, nv > 0 ? 8 : 0);
-        cp_async8(dst + 8, nv > 1 ? src + 1 : G, nv > 1 ? 8 : 0);
-      }
-    }
-  }
-}
 
 // Epilogues. kReadC: the accumulator starts from C (staged into shared memory by bulk async
 // copies, one tile ahead of its use); init() maps a C value to the initial accumulator and store2
@@ -91,6 +56,9 @@ struct EpiSub {  // C -= A.B   (acc = -C ; acc += A.B ; C = -acc : exact sign fl
   }
 };
 
+struct EpiStore;
+__device__ __forceinline__ double epi_diag(const struct EpiSub &) { return 0.0; }
+__device__ __forceinline__ double epi_diag(const EpiStore &e);
 struct EpiStore {  // C = A.B + diag_add * I
   static constexpr bool kReadC = false;
   double *C;
@@ -104,20 +72,13 @@ struct EpiStore {  // C = A.B + diag_add * I
   }
 };
 
-// Per-kernel shared state of the C-tile bulk-copy pipeline (one mbarrier, phase carried across calls).
+__device__ __forceinline__ double epi_diag(const EpiStore &e) { return e.diag_add; }
+
+// mbarriers of the gemm pipeline (re-initialised at every gemm call).
 struct GemmSync {
-  uint64_t cbar;
-  uint32_t cphase;
-  uint32_t pad;
+  uint64_t full[STAGES], empty[STAGES], cfull, cempty;
 };
-__device__ __forceinline__ void gemm_sync_init(GemmSync *gs) {
-  if (threadIdx.x == 0) {
-    mbar_init(&gs->cbar, 1);
-    gs->cphase = 0;
-    fence_barrier_init();
-  }
-  __syncthreads();
-}
+__device__ __forceinline__ void gemm_sync_init(GemmSync *) {}
 
 // Tile enumeration (row-major over tm); lower = only tiles holding some element with row >= col.
 __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
@@ -126,51 +87,62 @@ __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
   return min(tiles_n, last_col_tile + 1);
 }
 
-// Warp 0: bulk-copy the valid rows of C tile (tm, tn) into Cs (pitch CS_LD), completion on cbar.
-// Rows are copied as whole 16-byte chunks (may read <= 8 bytes past the last column: workspaces are
-// padded for this).
-__device__ __forceinline__ void issue_c_tile(const double *C, int64_t ldc, int M, int N, int tm,
-                                             int tn, double *Cs, uint64_t *cbar) {
-  const int lane = lane_id();
-  const int r0 = tm * BM, c0 = tn * BN;
-  const int rows = min(BM, M - r0), cols = min(BN, N - c0);
-  const uint32_t rb = static_cast<uint32_t>((cols * 8 + 15) & ~15);
-  if (lane == 0) mbar_arrive_expect_tx(cbar, rb * static_cast<uint32_t>(rows));
-  __syncwarp();
-  for (int r = lane; r < rows; r += 32)
-    bulk_g2s(smem_u32(Cs + r * CS_LD), C + static_cast<int64_t>(r0 + r) * ldc + c0, rb, cbar);
+__device__ __forceinline__ uint32_t round16(int bytes) { return static_cast<uint32_t>((bytes + 15) & ~15); }
+
+// Producer-warp helper: copy `nrows` rows of `rbytes` bytes (16-byte multiple) from
+// G + r*ld (r < nrows) to smem rows of pitch `ld_s` doubles; completion on bar.
+__device__ __forceinline__ void bulk_rows(double *s, int ld_s, const double *G, int64_t ld,
+                                          int nrows, uint32_t rbytes, uint64_t *bar) {
+  for (int r = lane_id(); r < nrows; r += 32)
+    bulk_g2s(smem_u32(s + r * ld_s), G + static_cast<int64_t>(r) * ld, rbytes, bar);
 }
 
-// C[M x N] op= A[M x K] . B[K x N] on the calling CTA. smem: GEMM_SMEM_DOUBLES doubles (A/B
-// double buffer for cp.async, plus the C tile buffer). Begins and ends with __syncthreads().
-// Pipeline: A/B k-slices (BK) double-buffered with cp.async groups; the next tile's C is fetched by
-// cp.async.bulk into Cs as soon as the current tile's accumulators have been initialised from it,
-// so its latency overlaps a whole tile of DMMA work.
-template <bool A_KC, bool B_KC, class Epi>
-__device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t lda, const double *B,
-                                  int64_t ldb, bool lower, double *smem, GemmSync *gs,
-                                  const Epi &epi) {
+// C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).
+//   A_KC: A element (m, k) at A[m*lda + k], else at A[k*lda + m]; likewise B_KC for (n, k).
+//   All of A, B (and C if the epilogue reads it) must be 16-byte aligned with even leading
+//   dimensions; tiles are moved by cp.async.bulk (rows of a tile rounded up to 16 bytes, so up
+//   to 8 bytes past a row end may be read: callers' buffers are padded).
+// Warp-specialised pipeline without CTA-wide barriers in the main loop: warp NCW (producer) streams
+// BK-deep A/B slices into a STAGES ring and each tile's C into a single C buffer (prefetched
+// while the previous tile is still computing); warps 0..NCW-1 run FP64 DMMA on 32x32 warp tiles
+// and store their part of the tile directly to global memory.
+struct GemmArgs {
+  const double *A, *B;
+  double *C;
+  int64_t lda, ldb, ldc;
+  int M, N, K;
+  bool a_kc, b_kc, lower, read_c;  // read_c: C -= A.B (else C = A.B + diag_add I)
+  double diag_add;
+};
+
+static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, GemmSync *gs) {
+  const double *A = ga.A, *B = ga.B;
+  const int64_t lda = ga.lda, ldb = ga.ldb;
+  const int M = ga.M, N = ga.N, K = ga.K;
+  const bool A_KC = ga.a_kc, B_KC = ga.b_kc, lower = ga.lower, readC = ga.read_c;
   __syncthreads();
-  if (M <= 0 || N <= 0) return;
+  if (M <= 0 || N <= 0 || K <= 0) {
+    // K == 0 only ever comes with EpiStore(0) in this library: nothing to accumulate
+    return;
+  }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&gs->full[st], 1);
+      mbar_init(&gs->empty[st], NCW);
+    }
+    mbar_init(&gs->cfull, 1);
+    mbar_init(&gs->cempty, NCW);
+    fence_barrier_init();
+  }
+  __syncthreads();
   const int tiles_m = cdiv(M, BM), tiles_n = cdiv(N, BN);
-  const int nkc = K > 0 ? cdiv(K, BK) : 1;
+  const int nkc = cdiv(K, BK);
   int ntiles = 0;
   for (int tm = 0; tm < tiles_m; ++tm) ntiles += tiles_in_row(tm, tiles_n, lower);
   const int total = ntiles * nkc;
-  const bool al16 = ((lda | ldb) & 1) == 0 &&
-                    ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
-  bool bulk_c = false;
-  if constexpr (Epi::kReadC)
-    bulk_c = (epi.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(epi.C) & 15) == 0;
-  double *As[2] = {smem, smem + A_ELEMS};
-  double *Bs[2] = {smem + 2 * A_ELEMS, smem + 2 * A_ELEMS + B_ELEMS};
-  double *Cs = smem + 2 * (A_ELEMS + B_ELEMS);
-  uint32_t ph = gs->cphase;
-
-  const int warp = warp_id(), lane = lane_id();
-  const int wm = warp % WM, wn = warp / WM;
-  const int g = lane >> 2, t = lane & 3;
-
+  double *Cs = smem + STAGES * (A_ELEMS + B_ELEMS);
+  auto As = [&](int st) { return smem + st * (A_ELEMS + B_ELEMS); };
+  auto Bs = [&](int st) { return smem + st * (A_ELEMS + B_ELEMS) + A_ELEMS; };
   auto decode_tile = [&](int tile, int &tm, int &tn) {
     tm = 0;
     int cnt;
@@ -180,104 +152,176 @@ __device__ __noinline__ void gemm(int M, int N, int K, const double *A, int64_t 
     }
     tn = tile;
   };
-  auto issue_ab = [&](int it) {
-    int tm, tn;
-    decode_tile(it / nkc, tm, tn);
-    const int kc = it % nkc, buf = it & 1;
-    stage_operand<A_KC, BM>(As[buf], A, lda, tm * BM, kc * BK, M, K, al16);
-    stage_operand<B_KC, BN>(Bs[buf], B, ldb, tn * BN, kc * BK, N, K, al16);
-    cp_async_commit();
-  };
+  const int warp = warp_id(), lane = lane_id();
 
-  if (bulk_c && warp == 0) {
-    int tm, tn;
-    decode_tile(0, tm, tn);
-    issue_c_tile(epi.C, epi.ldc, M, N, tm, tn, Cs, &gs->cbar);
-  }
-  issue_ab(0);
-  double acc[MI][NI][2];
-  for (int it = 0; it < total; ++it) {
-    const int tile = it / nkc, kc = it % nkc;
-    int tm, tn;
-    decode_tile(tile, tm, tn);
-    if (it + 1 < total) issue_ab(it + 1);
-    if (kc == 0) {
-      if (bulk_c) {
-        mbar_wait(&gs->cbar, ph);
-        ph ^= 1;
+  if (warp == NCW) {
+    // ============================ producer warp ============================
+    // generic-proxy global writes of earlier phases (made CTA-visible by the barrier above) must be
+    // ordered before this warp's async-proxy bulk reads
+    asm volatile("fence.proxy.async;\n" ::: "memory");
+    for (int it = 0; it < total; ++it) {
+      const int st = it % STAGES, use = it / STAGES;
+      const int tile = it / nkc, kc = it % nkc;
+      int tm, tn;
+      decode_tile(tile, tm, tn);
+      if (kc == 0 && readC) {
+        if (tile > 0) mbar_wait(&gs->cempty, (tile - 1) & 1);
+        const int rows = min(BM, M - tm * BM), cols = min(BN, N - tn * BN);
+        const uint32_t rb = round16(cols * 8);
+        if (lane == 0) mbar_arrive_expect_tx(&gs->cfull, rb * rows);
+        __syncwarp();
+        bulk_rows(Cs, CS_LD, ga.C + static_cast<int64_t>(tm * BM) * ga.ldc + tn * BN, ga.ldc, rows,
+                  rb, &gs->cfull);
       }
+      if (it >= STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
+      const int k0 = kc * BK, krem = min(BK, K - k0);
+      const int ra = min(BM, M - tm * BM), rbn = min(BN, N - tn * BN);
+      const uint32_t a_rb = A_KC ? round16(krem * 8) : round16(ra * 8);
+      const int a_nr = A_KC ? ra : krem;
+      const uint32_t b_rb = B_KC ? round16(krem * 8) : round16(rbn * 8);
+      const int b_nr = B_KC ? rbn : krem;
+      if (lane == 0) mbar_arrive_expect_tx(&gs->full[st], a_rb * a_nr + b_rb * b_nr);
+      __syncwarp();
+      if (A_KC)
+        bulk_rows(As(st), KC_LD, A + static_cast<int64_t>(tm * BM) * lda + k0, lda, a_nr, a_rb,
+                  &gs->full[st]);
+      else
+        bulk_rows(As(st), A_MC_LD, A + static_cast<int64_t>(k0) * lda + tm * BM, lda, a_nr, a_rb,
+                  &gs->full[st]);
+      if (B_KC)
+        bulk_rows(Bs(st), KC_LD, B + static_cast<int64_t>(tn * BN) * ldb + k0, ldb, b_nr, b_rb,
+                  &gs->full[st]);
+      else
+        bulk_rows(Bs(st), B_NC_LD, B + static_cast<int64_t>(k0) * ldb + tn * BN, ldb, b_nr, b_rb,
+                  &gs->full[st]);
+    }
+  } else {
+    // ============================ consumer warps ============================
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t = lane & 3;
+    double acc[MI][NI][2];
+    for (int it = 0; it < total; ++it) {
+      const int st = it % STAGES, use = it / STAGES;
+      const int tile = it / nkc, kc = it % nkc;
+      int tm, tn;
+      decode_tile(tile, tm, tn);
+      if (kc == 0) {
+        if (readC) {
+          mbar_wait(&gs->cfull, tile & 1);
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) {
-        const int rl = wm * WTM + mi * 8 + g;
-        const int r = tm * BM + rl;
+          for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          const int cl = wn * WTN + ni * 8 + 2 * t;
-          const int c = tn * BN + cl;
-          double c0v = 0.0, c1v = 0.0;
-          if constexpr (Epi::kReadC) {
-            if (bulk_c) {
-              c0v = Cs[rl * CS_LD + cl];
-              c1v = Cs[rl * CS_LD + cl + 1];
-            } else {
-              const double *p = epi.C + static_cast<int64_t>(r) * epi.ldc + c;
-              if (r < M && c < N) c0v = p[0];
-              if (r < M && c + 1 < N) c1v = p[1];
+            for (int ni = 0; ni < NI; ++ni) {
+              double c0, c1;
+              lds128(c0, c1, smem_u32(Cs + (wm * WTM + mi * 8 + g) * CS_LD + wn * WTN + ni * 8 + 2 * t));
+              acc[mi][ni][0] = -c0;  // C -= A.B as acc = -C; acc += A.B; C = -acc (exact)
+              acc[mi][ni][1] = -c1;
             }
-          }
-          acc[mi][ni][0] = epi.init(c0v);
-          acc[mi][ni][1] = epi.init(c1v);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&gs->cempty);
+        } else {
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
         }
       }
-    }
-    if (it + 1 < total)
-      cp_async_wait<1>();
-    else
-      cp_async_wait<0>();
-    __syncthreads();
-    if (kc == 0 && bulk_c && tile + 1 < ntiles && warp == 0) {
-      int tm2, tn2;
-      decode_tile(tile + 1, tm2, tn2);
-      fence_proxy_async();
-      issue_c_tile(epi.C, epi.ldc, M, N, tm2, tn2, Cs, &gs->cbar);
-    }
-    if (K > 0) {
-      const double *as = As[it & 1], *bs = Bs[it & 1];
-#pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
-        const int k = ks * 4 + t;
-        double a[MI], b[NI];
+      mbar_wait(&gs->full[st], use & 1);
+      const int krem = min(BK, K - kc * BK);
+      const double *as = As(st), *bs = Bs(st);
+#pragma unroll 1
+      for (int k8 = 0; k8 < BK / 8; ++k8) {
+        if (k8 * 8 >= krem) break;
+        const int k = k8 * 8 + 2 * t;  // this lane's k pair (k, k+1) for the two DMMAs
+        double a[MI][2], b[NI][2];
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
           const int m = wm * WTM + mi * 8 + g;
-          a[mi] = A_KC ? as[m * (BK + 4) + k] : as[k * (BM + 4) + m];
+          if (A_KC) {
+            lds128(a[mi][0], a[mi][1], smem_u32(as + m * KC_LD + k));
+          } else {
+            a[mi][0] = as[k * A_MC_LD + m];
+            a[mi][1] = as[(k + 1) * A_MC_LD + m];
+          }
         }
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) {
           const int n = wn * WTN + ni * 8 + g;
-          b[ni] = B_KC ? bs[n * (BK + 4) + k] : bs[k * (BN + 4) + n];
+          if (B_KC) {
+            lds128(b[ni][0], b[ni][1], smem_u32(bs + n * KC_LD + k));
+          } else {
+            b[ni][0] = bs[k * B_NC_LD + n];
+            b[ni][1] = bs[(k + 1) * B_NC_LD + n];
+          }
+        }
+        if (k8 * 8 + 8 > krem) {  // partial slice: zero both operands beyond K (stale smem)
+          const bool v0 = k < krem, v1 = k + 1 < krem;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) {
+            a[mi][0] = v0 ? a[mi][0] : 0.0;
+            a[mi][1] = v1 ? a[mi][1] : 0.0;
+          }
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) {
+            b[ni][0] = v0 ? b[ni][0] : 0.0;
+            b[ni][1] = v1 ? b[ni][1] : 0.0;
+          }
         }
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+          for (int ni = 0; ni < NI; ++ni) {
+            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][0], b[ni][0]);
+            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][1], b[ni][1]);
+          }
       }
-    }
-    __syncthreads();
-    if (kc == nkc - 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gs->empty[st]);
+      if (kc == nkc - 1) {
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) {
-        const int r = tm * BM + wm * WTM + mi * 8 + g;
+        for (int mi = 0; mi < MI; ++mi) {
+          const int r = tm * BM + wm * WTM + mi * 8 + g;
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          const int c = tn * BN + wn * WTN + ni * 8 + 2 * t;
-          epi.store2(r, c, r < M && c < N, r < M && c + 1 < N, acc[mi][ni][0], acc[mi][ni][1]);
+          for (int ni = 0; ni < NI; ++ni) {
+            const int c = tn * BN + wn * WTN + ni * 8 + 2 * t;
+            const bool v0 = r < M && c < N, v1 = r < M && c + 1 < N;
+            double *p = ga.C + static_cast<int64_t>(r) * ga.ldc + c;
+            if (readC) {
+              if (v0) p[0] = -acc[mi][ni][0];
+              if (v1) p[1] = -acc[mi][ni][1];
+            } else {
+              if (v0) p[0] = acc[mi][ni][0] + (r == c ? ga.diag_add : 0.0);
+              if (v1) p[1] = acc[mi][ni][1] + (r == c + 1 ? ga.diag_add : 0.0);
+            }
+          }
         }
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) gs->cphase = ph;
+}
+
+// Typed front end: builds the runtime argument block (one compiled instance of the pipeline).
+template <bool A_KC, bool B_KC, class Epi>
+__device__ __forceinline__ void gemm(int M, int N, int K, const double *A, int64_t lda, const double *B,
+                                     int64_t ldb, bool lower, double *smem, GemmSync *gs,
+                                     const Epi &epi) {
+  GemmArgs ga;
+  ga.A = A;
+  ga.B = B;
+  ga.C = epi.C;
+  ga.lda = lda;
+  ga.ldb = ldb;
+  ga.ldc = epi.ldc;
+  ga.M = M;
+  ga.N = N;
+  ga.K = K;
+  ga.a_kc = A_KC;
+  ga.b_kc = B_KC;
+  ga.lower = lower;
+  ga.read_c = Epi::kReadC;
+  ga.diag_add = Epi::kReadC ? 0.0 : epi_diag(epi);
+  gemm_rt(ga, smem, gs);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -317,7 +361,7 @@ __device__ __forceinline__ void block_argmax(double &v, int &idx, double *redv, 
 // are also recorded in ipiv[0..bw). Returns 1 on an exact zero pivot. The rank-1 update of column
 // j is fused with the pivot search of column j+1 (one pass over the rows per column).
 // Pivot rule: max |a_ij|, ties -> lowest row (the oracle's rule).
-static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0, int bw, int sc0,
+__device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, int bw, int sc0,
                                             int sc1, int *ipiv, double *redv, int *redi) {
   const int warp = warp_id(), lane = lane_id();
   int singular = 0;
@@ -403,60 +447,54 @@ static __device__ __noinline__ int panel_lu(double *M, int64_t ld, int n, int p0
   return singular;
 }
 
-// U12 = L11^{-1} A12 for the rows [p0, p0+bw) and columns [c0, c1), L11 = unit lower part of
-// M[p0:p0+bw, p0:p0+bw] (bw <= 32). One thread per column.
-static __device__ __noinline__ void trsm_unit_lower_cols(double *M, int64_t ld, int p0, int bw,
-                                                         int c0, int c1, double *tri) {
+// Inverse of a bw x bw (bw <= PB) triangular diagonal block src[p0.., p0..] written to the global
+// scratch Tg [PB][PB] (zero padded), so that every triangular solve of the factorizations becomes a
+// DMMA GEMM with this inverse (MAGMA-style inverted diagonal blocks).
+//   kind 0: unit lower (strict lower part of src)   kind 1: lower (non-unit)   kind 2: upper (non-unit)
+// All threads stage the block into smem; warp 0 computes column c of the inverse in lane c by
+// substitution (registers, fixed-size unrolled loops); all threads then write Tg.
+enum { TRI_UNIT_LOWER = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
+__device__ __forceinline__ void tri_inv(const double *src, int64_t ld, int p0, int bw, int kind,
+                                        double *tri, double *Tg) {
+  __syncthreads();
   for (int q = threadIdx.x; q < PB * PB; q += NT) {
     const int r = q / PB, c = q % PB;
-    tri[r * TRI_LD + c] = (r < bw && c < r) ? M[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
-  }
-  __syncthreads();
-  for (int c = c0 + threadIdx.x; c < c1; c += NT) {
-    double x[PB];
-#pragma unroll
-    for (int r = 0; r < PB; ++r) x[r] = r < bw ? M[static_cast<int64_t>(p0 + r) * ld + c] : 0.0;
-#pragma unroll
-    for (int r = 1; r < PB; ++r) {
-      double s = x[r];
-#pragma unroll
-      for (int q = 0; q < r; ++q) s = fma(-tri[r * TRI_LD + q], x[q], s);
-      x[r] = s;
+    double v = 0.0;
+    if (r < bw && c < bw) {
+      const bool keep = kind == TRI_UPPER ? (c >= r) : (kind == TRI_LOWER ? (c <= r) : (c < r));
+      if (keep) v = src[static_cast<int64_t>(p0 + r) * ld + p0 + c];
     }
-#pragma unroll
-    for (int r = 0; r < PB; ++r)
-      if (r < bw) M[static_cast<int64_t>(p0 + r) * ld + c] = x[r];
+    if (kind == TRI_UNIT_LOWER && r == c) v = 1.0;
+    if (r >= bw && r == c) v = 1.0;  // identity padding keeps the unrolled substitution finite
+    tri[r * TRI_LD + c] = v;
   }
   __syncthreads();
-}
-
-// X[p0:p0+bw, c0:c1) = U^{-1} X for the upper-triangular (non-unit) U = M[p0:p0+bw, p0:p0+bw];
-// X lives at Xb + r*ldx + c (row r relative to p0 in the same row numbering). Thread per column.
-static __device__ __noinline__ void trsm_upper_cols(const double *M, int64_t ld, int p0, int bw, double *Xb,
-                                int64_t ldx, int ncols, double *tri) {
-  for (int q = threadIdx.x; q < bw * bw; q += NT) {
-    const int r = q / bw, c = q % bw;
-    tri[r * TRI_LD + c] = M[static_cast<int64_t>(p0 + r) * ld + p0 + c];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < ncols; c += NT) {
+  if (warp_id() == 0) {
+    const int c = lane_id();
     double x[PB];
+    if (kind != TRI_UPPER) {
 #pragma unroll
-    for (int r = 0; r < PB; ++r) x[r] = r < bw ? Xb[static_cast<int64_t>(p0 + r) * ldx + c] : 0.0;
+      for (int r = 0; r < PB; ++r) {
+        double s = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-    for (int r = PB - 1; r >= 0; --r) {
-      if (r < bw) {
-        double s = x[r];
+        for (int q = 0; q < r; ++q) s = fma(-tri[r * TRI_LD + q], x[q], s);
+        x[r] = (kind == TRI_LOWER) ? s / tri[r * TRI_LD + r] : s;
+      }
+    } else {
 #pragma unroll
-        for (int q = r + 1; q < PB; ++q)
-          if (q < bw) s = fma(-tri[r * TRI_LD + q], x[q], s);
+      for (int r = PB - 1; r >= 0; --r) {
+        double s = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = r + 1; q < PB; ++q) s = fma(-tri[r * TRI_LD + q], x[q], s);
         x[r] = s / tri[r * TRI_LD + r];
       }
     }
+    __syncwarp();
 #pragma unroll
-    for (int r = 0; r < PB; ++r)
-      if (r < bw) Xb[static_cast<int64_t>(p0 + r) * ldx + c] = x[r];
+    for (int r = 0; r < PB; ++r) tri[r * TRI_LD + c] = (r < bw && c < bw) ? x[r] : 0.0;
   }
+  __syncthreads();
+  for (int q = threadIdx.x; q < PB * PB; q += NT) Tg[q] = tri[(q / PB) * TRI_LD + (q % PB)];
   __syncthreads();
 }
 
@@ -470,80 +508,9 @@ __device__ __forceinline__ void load_lower_tri(const double *S, int64_t ld, int 
   __syncthreads();
 }
 
-// X[p0:p0+bw, :] = L^{-1} X  (L lower non-unit in tri). Thread per column.
-static __device__ __noinline__ void trsm_lower_cols(const double *tri, int bw, double *X, int64_t ldx, int p0,
-                                int ncols) {
-  for (int c = threadIdx.x; c < ncols; c += NT) {
-    double x[PB];
-#pragma unroll
-    for (int r = 0; r < PB; ++r) x[r] = r < bw ? X[static_cast<int64_t>(p0 + r) * ldx + c] : 0.0;
-#pragma unroll
-    for (int r = 0; r < PB; ++r) {
-      if (r < bw) {
-        double s = x[r];
-#pragma unroll
-        for (int q = 0; q < r; ++q) s = fma(-tri[r * TRI_LD + q], x[q], s);
-        x[r] = s / tri[r * TRI_LD + r];
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < PB; ++r)
-      if (r < bw) X[static_cast<int64_t>(p0 + r) * ldx + c] = x[r];
-  }
-  __syncthreads();
-}
-
-// X[p0:p0+bw, :] = L^{-T} X  (L lower non-unit in tri). Thread per column.
-static __device__ __noinline__ void trsm_lower_t_cols(const double *tri, int bw, double *X, int64_t ldx, int p0,
-                                  int ncols) {
-  for (int c = threadIdx.x; c < ncols; c += NT) {
-    double x[PB];
-#pragma unroll
-    for (int r = 0; r < PB; ++r) x[r] = r < bw ? X[static_cast<int64_t>(p0 + r) * ldx + c] : 0.0;
-#pragma unroll
-    for (int r = PB - 1; r >= 0; --r) {
-      if (r < bw) {
-        double s = x[r];
-#pragma unroll
-        for (int q = r + 1; q < PB; ++q)
-          if (q < bw) s = fma(-tri[q * TRI_LD + r], x[q], s);
-        x[r] = s / tri[r * TRI_LD + r];
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < PB; ++r)
-      if (r < bw) X[static_cast<int64_t>(p0 + r) * ldx + c] = x[r];
-  }
-  __syncthreads();
-}
-
-// Rows [r0, r1) of the panel S[:, p0:p0+bw]: L21 = S21 L11^{-T} (L11 lower in tri). Thread per row.
-static __device__ __noinline__ void trsm_rows_lt(const double *tri, int bw, double *S, int64_t ld, int p0, int r0,
-                             int r1) {
-  for (int r = r0 + threadIdx.x; r < r1; r += NT) {
-    double *row = S + static_cast<int64_t>(r) * ld + p0;
-    double x[PB];
-#pragma unroll
-    for (int c = 0; c < PB; ++c) x[c] = c < bw ? row[c] : 0.0;
-#pragma unroll
-    for (int c = 0; c < PB; ++c) {
-      if (c < bw) {
-        double s = x[c];
-#pragma unroll
-        for (int q = 0; q < c; ++q) s = fma(-x[q], tri[c * TRI_LD + q], s);
-        x[c] = s / tri[c * TRI_LD + c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < PB; ++c)
-      if (c < bw) row[c] = x[c];
-  }
-  __syncthreads();
-}
-
 // Unblocked Cholesky of S[p0:p0+bw, p0:p0+bw] (lower) in tri, written back to S.
 // Returns 1 if a non-positive pivot appears (S is SPD by construction: I + K K^T).
-static __device__ __noinline__ int chol_diag(double *S, int64_t ld, int p0, int bw, double *tri) {
+__device__ __forceinline__ int chol_diag(double *S, int64_t ld, int p0, int bw, double *tri) {
   load_lower_tri(S, ld, p0, bw, tri);
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;

@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(NT, 1)
   gemm_sync_init(&sm.gs);
   double *Mw = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
   const int npad = (n + 1) & ~1;
+  double *Tg = Mw + static_cast<int64_t>(n) * ldm + 32;  // PB x PB inverse of a diagonal block
   auto Mp = [&](int r, int c) { return Mw + static_cast<int64_t>(r) * ldm + c; };
 
   for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
@@ -83,46 +84,62 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
 
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
+    // Triangular solves with the 32x32 diagonal blocks run as in-place DMMA GEMMs with their
+    // explicit inverses (Tg); every operand stays in the slot workspace (aligned, even pitch).
     int singular = 0;
     for (int P0 = 0; P0 < n; P0 += NB) {
       const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
       singular |= panel_lu(Mw, ldm, n, P0, w1, P0, ncols, sm.ipiv, sm.redv, sm.redi);
+      tri_inv(Mw, ldm, P0, w1, TRI_UNIT_LOWER, sm.tri, Tg);  // L_aa^{-1}
       if (w2 > 0) {
-        // right half of the outer block: U_ab = L_aa^{-1} A_ab, then A_bb.. -= L_.a U_ab
-        trsm_unit_lower_cols(Mw, ldm, P0, w1, P0 + w1, P0 + W, sm.tri);
+        // right half of the outer block: U_ab = L_aa^{-1} A_ab ; A_.b -= L_.a U_ab ; factor it
+        gemm<true, false>(w1, w2, w1, Tg, PB, Mp(P0, P0 + w1), ldm, false, sm.gemm, &sm.gs,
+                          EpiStore{Mp(P0, P0 + w1), ldm, 0.0});
         gemm<true, false>(n - P0 - w1, w2, w1, Mp(P0 + w1, P0), ldm, Mp(P0, P0 + w1), ldm, false,
                           sm.gemm, &sm.gs, EpiSub{Mp(P0 + w1, P0 + w1), ldm});
         singular |= panel_lu(Mw, ldm, n, P0 + w1, w2, P0, ncols, sm.ipiv + PB, sm.redv, sm.redi);
       }
-      if (P0 + W < ncols) {
-        // U12 = L11^{-1} A12 over the trailing columns, L11 = [[L_aa, 0], [L_ba, L_bb]]
-        trsm_unit_lower_cols(Mw, ldm, P0, w1, P0 + W, ncols, sm.tri);
+      // trailing columns (A part and right-hand sides); when the last block ends on an odd n the
+      // zero pad column n is skipped so that every tile row stays 16-byte aligned
+      const int ct = min((P0 + W + 1) & ~1, ncols);
+      const int nt = ncols - ct;
+      if (nt > 0) {
+        // U12 = L11^{-1} A12, L11 = [[L_aa, 0], [L_ba, L_bb]]
+        gemm<true, false>(w1, nt, w1, Tg, PB, Mp(P0, ct), ldm, false, sm.gemm, &sm.gs,
+                          EpiStore{Mp(P0, ct), ldm, 0.0});
         if (w2 > 0) {
-          gemm<true, false>(w2, ncols - P0 - W, w1, Mp(P0 + w1, P0), ldm, Mp(P0, P0 + W), ldm, false,
-                            sm.gemm, &sm.gs, EpiSub{Mp(P0 + w1, P0 + W), ldm});
-          trsm_unit_lower_cols(Mw, ldm, P0 + w1, w2, P0 + W, ncols, sm.tri);
+          gemm<true, false>(w2, nt, w1, Mp(P0 + w1, P0), ldm, Mp(P0, ct), ldm, false, sm.gemm,
+                            &sm.gs, EpiSub{Mp(P0 + w1, ct), ldm});
+          tri_inv(Mw, ldm, P0 + w1, w2, TRI_UNIT_LOWER, sm.tri, Tg);  // L_bb^{-1}
+          gemm<true, false>(w2, nt, w2, Tg, PB, Mp(P0 + w1, ct), ldm, false, sm.gemm, &sm.gs,
+                            EpiStore{Mp(P0 + w1, ct), ldm, 0.0});
         }
         // trailing update with K = W
         if (P0 + W < n)
-          gemm<true, false>(n - P0 - W, ncols - P0 - W, W, Mp(P0 + W, P0), ldm, Mp(P0, P0 + W), ldm,
-                            false, sm.gemm, &sm.gs, EpiSub{Mp(P0 + W, P0 + W), ldm});
+          gemm<true, false>(n - P0 - W, nt, W, Mp(P0 + W, P0), ldm, Mp(P0, ct), ldm, false,
+                            sm.gemm, &sm.gs, EpiSub{Mp(P0 + W, ct), ldm});
       }
     }
 
     // ---- S4b: blocked back substitution U Y = L^{-1} P B_open (Y in columns [npad, npad+o)) ----
     if (o > 0) {
       double *Y = Mw + npad;
+      auto Yr = [&](int r) { return Y + static_cast<int64_t>(r) * ldm; };
       for (int P0 = ((n - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
         const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
         if (w2 > 0) {
-          trsm_upper_cols(Mw, ldm, P0 + w1, w2, Y, ldm, o, sm.tri);
-          gemm<true, false>(w1, o, w2, Mp(P0, P0 + w1), ldm, Y + static_cast<int64_t>(P0 + w1) * ldm,
-                            ldm, false, sm.gemm, &sm.gs, EpiSub{Y + static_cast<int64_t>(P0) * ldm, ldm});
+          tri_inv(Mw, ldm, P0 + w1, w2, TRI_UPPER, sm.tri, Tg);  // U_bb^{-1}
+          gemm<true, false>(w2, o, w2, Tg, PB, Yr(P0 + w1), ldm, false, sm.gemm, &sm.gs,
+                            EpiStore{Yr(P0 + w1), ldm, 0.0});
+          gemm<true, false>(w1, o, w2, Mp(P0, P0 + w1), ldm, Yr(P0 + w1), ldm, false, sm.gemm,
+                            &sm.gs, EpiSub{Yr(P0), ldm});
         }
-        trsm_upper_cols(Mw, ldm, P0, w1, Y, ldm, o, sm.tri);
+        tri_inv(Mw, ldm, P0, w1, TRI_UPPER, sm.tri, Tg);  // U_aa^{-1}
+        gemm<true, false>(w1, o, w1, Tg, PB, Yr(P0), ldm, false, sm.gemm, &sm.gs,
+                          EpiStore{Yr(P0), ldm, 0.0});
         if (P0 > 0)
-          gemm<true, false>(P0, o, W, Mp(0, P0), ldm, Y + static_cast<int64_t>(P0) * ldm, ldm, false,
-                            sm.gemm, &sm.gs, EpiSub{Y, ldm});
+          gemm<true, false>(P0, o, W, Mp(0, P0), ldm, Yr(P0), ldm, false, sm.gemm, &sm.gs,
+                            EpiSub{Y, ldm});
       }
     }
 
@@ -157,7 +174,8 @@ size_t match_smem_bytes() { return sizeof(MatchSmem); }
 
 int64_t match_ws_doubles_per_slot(int64_t nch) {
   const int64_t npad = (nch + 1) & ~1LL;
-  return nch * (2 * npad) + 32;  // + tail padding for 16-byte bulk copies of odd-width C tiles
+  // M [n][2 npad] + tail padding for 16-byte bulk copies + the PB x PB diagonal-block inverse
+  return nch * (2 * npad) + 32 + 32 * 32 + 32;
 }
 
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,

@@ -30,6 +30,8 @@ __global__ void __launch_bounds__(NT, 1)
   gemm_sync_init(&sm.gs);
   double *S = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;  // o x ldo; later holds P
   double *X = S + static_cast<int64_t>(n) * ldo;                // o x ldo
+  double *Kc = X + static_cast<int64_t>(n) * ldo;               // o x ldo: aligned copy of K_oo
+  double *Tg = Kc + static_cast<int64_t>(n) * ldo + 32;          // PB x PB diagonal-block inverse
   auto Sp = [&](int r, int c) { return S + static_cast<int64_t>(r) * ldo + c; };
   auto Xr = [&](int r) { return X + static_cast<int64_t>(r) * ldo; };
 
@@ -44,18 +46,33 @@ __global__ void __launch_bounds__(NT, 1)
     }
     int bad = 0;
     if (o > 0) {
+      // Kc = X = K_oo (16-byte aligned, even pitch: operands of the bulk-copy GEMM pipeline)
+      for (int i = warp_id(); i < o; i += NW)
+        for (int j = lane_id(); j < o; j += 32) {
+          const double v = Ke[static_cast<int64_t>(i) * ldk + j];
+          Kc[static_cast<int64_t>(i) * ldo + j] = v;
+          Xr(i)[j] = v;
+        }
+      __syncthreads();
       // S = I + K_oo K_oo^T (lower tiles)
-      gemm<true, true>(o, o, o, Ke, ldk, Ke, ldk, true, sm.gemm, &sm.gs, EpiStore{S, ldo, 1.0});
-      // blocked Cholesky S = L L^T (lower)
+      gemm<true, true>(o, o, o, Kc, ldo, Kc, ldo, true, sm.gemm, &sm.gs, EpiStore{S, ldo, 1.0});
+      // blocked Cholesky S = L L^T (lower); panel solves L21 = S21 L11^{-T} as in-place GEMMs
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
         bad |= chol_diag(S, ldo, P0, w1, sm.tri);
-        if (P0 + w1 < o) trsm_rows_lt(sm.tri, w1, S, ldo, P0, P0 + w1, o);
+        tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
+        if (P0 + w1 < o)
+          gemm<true, true>(o - P0 - w1, w1, w1, Sp(P0 + w1, P0), ldo, Tg, PB, false, sm.gemm, &sm.gs,
+                           EpiStore{Sp(P0 + w1, P0), ldo, 0.0});
         if (w2 > 0) {
           gemm<true, true>(o - P0 - w1, w2, w1, Sp(P0 + w1, P0), ldo, Sp(P0 + w1, P0), ldo, false,
                            sm.gemm, &sm.gs, EpiSub{Sp(P0 + w1, P0 + w1), ldo});
           bad |= chol_diag(S, ldo, P0 + w1, w2, sm.tri);
-          if (P0 + W < o) trsm_rows_lt(sm.tri, w2, S, ldo, P0 + w1, P0 + W, o);
+          if (P0 + W < o) {
+            tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
+            gemm<true, true>(o - P0 - W, w2, w2, Sp(P0 + W, P0 + w1), ldo, Tg, PB, false, sm.gemm,
+                             &sm.gs, EpiStore{Sp(P0 + W, P0 + w1), ldo, 0.0});
+          }
         }
         if (P0 + W < o) {
           const int m2 = o - P0 - W;
@@ -63,20 +80,17 @@ __global__ void __launch_bounds__(NT, 1)
                            EpiSub{Sp(P0 + W, P0 + W), ldo});
         }
       }
-      // X = K_oo
-      for (int i = warp_id(); i < o; i += NW)
-        for (int j = lane_id(); j < o; j += 32) Xr(i)[j] = Ke[static_cast<int64_t>(i) * ldk + j];
-      __syncthreads();
-      // forward: L Z = K
+      // forward: L Z = K  (X holds K_oo)
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
-        load_lower_tri(S, ldo, P0, w1, sm.tri);
-        trsm_lower_cols(sm.tri, w1, X, ldo, P0, o);
+        tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
+        gemm<true, false>(w1, o, w1, Tg, PB, Xr(P0), ldo, false, sm.gemm, &sm.gs, EpiStore{Xr(P0), ldo, 0.0});
         if (w2 > 0) {
           gemm<true, false>(w2, o, w1, Sp(P0 + w1, P0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
                             EpiSub{Xr(P0 + w1), ldo});
-          load_lower_tri(S, ldo, P0 + w1, w2, sm.tri);
-          trsm_lower_cols(sm.tri, w2, X, ldo, P0 + w1, o);
+          tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
+          gemm<true, false>(w2, o, w2, Tg, PB, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
+                            EpiStore{Xr(P0 + w1), ldo, 0.0});
         }
         if (P0 + W < o)
           gemm<true, false>(o - P0 - W, o, W, Sp(P0 + W, P0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
@@ -86,21 +100,23 @@ __global__ void __launch_bounds__(NT, 1)
       for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
         const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
         if (w2 > 0) {
-          load_lower_tri(S, ldo, P0 + w1, w2, sm.tri);
-          trsm_lower_t_cols(sm.tri, w2, X, ldo, P0 + w1, o);
-          // X[P0:P0+w1] -= (L[P0+w1:P0+W, P0:P0+w1])^T X[P0+w1:P0+W]; A(i,k) = S[(P0+w1+k), P0+i]
+          tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
+          // X_b = L_bb^{-T} X_b : A(m,k) = Tg[k][m] -> [K][M]
+          gemm<false, false>(w2, o, w2, Tg, PB, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
+                             EpiStore{Xr(P0 + w1), ldo, 0.0});
+          // X_a -= (L[P0+w1:P0+W, P0:P0+w1])^T X_b
           gemm<false, false>(w1, o, w2, Sp(P0 + w1, P0), ldo, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
                              EpiSub{Xr(P0), ldo});
         }
-        load_lower_tri(S, ldo, P0, w1, sm.tri);
-        trsm_lower_t_cols(sm.tri, w1, X, ldo, P0, o);
+        tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
+        gemm<false, false>(w1, o, w1, Tg, PB, Xr(P0), ldo, false, sm.gemm, &sm.gs, EpiStore{Xr(P0), ldo, 0.0});
         if (P0 > 0)
           // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]; A(i,k) = S[(P0+k)*ldo + i] -> [K][M]
           gemm<false, false>(P0, o, W, Sp(P0, 0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
                              EpiSub{X, ldo});
       }
       // P = K_oo X  (into S's storage)
-      gemm<true, false>(o, o, o, Ke, ldk, X, ldo, false, sm.gemm, &sm.gs, EpiStore{S, ldo, 0.0});
+      gemm<true, false>(o, o, o, Kc, ldo, X, ldo, false, sm.gemm, &sm.gs, EpiStore{S, ldo, 0.0});
     }
     // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
@@ -127,7 +143,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 int64_t tepi_ws_doubles_per_slot(int64_t nch) {
   const int64_t npad = (nch + 1) & ~1LL;
-  return 2 * nch * npad + 32;  // + tail padding for 16-byte bulk copies of odd-width C tiles
+  return 3 * nch * npad + 32 + 32 * 32 + 32;  // + tail padding for 16-byte bulk copies of odd-width C tiles
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
