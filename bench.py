@@ -191,8 +191,10 @@ def main():
     my_blocks = rdist.cyclic_blocks(ne, batch, world, rank)
     nsteps = args.warmup + args.steps
 
+    # Steps walk this rank's blocks spread evenly over the whole mesh (not just its first blocks),
+    # so a short run sees the same mix of open-channel counts n_o(E) as the full sweep.
     def block_of_step(s):
-        return my_blocks[s % len(my_blocks)]
+        return my_blocks[min(len(my_blocks) - 1, int((s + 0.5) * len(my_blocks) / nsteps))]
 
     step_inputs = []
     for s in range(nsteps):

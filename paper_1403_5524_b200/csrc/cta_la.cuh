@@ -17,7 +17,7 @@
 namespace rmx {
 namespace la {
 
-constexpr int NT = 288;  // threads per CTA: 8 DMMA consumer warps + 1 copy-producer warp
+constexpr int NT = 288;  // threads per CTA: 8 DMMA consumer warps + 1 TMA-producer warp
 constexpr int NW = NT / 32;
 constexpr int NCW = 8;          // consumer warps inside gemm(); warp NCW is the producer
 constexpr int BM = 128, BN = 64, BK = 32, WM = 4, WN = 2;
@@ -25,60 +25,48 @@ constexpr int WTM = BM / WM, WTN = BN / WN;  // 32 x 32 warp tile
 constexpr int MI = WTM / 8, NI = WTN / 8;    // 4 x 4 DMMA fragments
 constexpr int PB = 32;                        // inner panel / triangle width of the factorizations
 constexpr int NB = 2 * PB;                    // outer block width (K of the big trailing GEMMs)
-constexpr int STAGES = 2;                     // A/B ring depth
-// smem pitches (doubles), chosen for conflict-free fragment loads:
-//   k-contiguous tiles [rows][KC_LD]   : 16-byte LDS of (k, k+1), row stride = 64 mod 128 bytes
-//   m/n-contiguous tiles [k][X_LD]     : 8-byte LDS, 4*ld = 8 mod 32 banks
-constexpr int KC_LD = BK + 8;
-constexpr int A_MC_LD = BM + 2, B_NC_LD = BN + 2;
-constexpr int A_ELEMS = (BM * KC_LD > BK * A_MC_LD) ? BM * KC_LD : BK * A_MC_LD;
-constexpr int B_ELEMS = (BN * KC_LD > BK * B_NC_LD) ? BN * KC_LD : BK * B_NC_LD;
-constexpr int CS_LD = BN + 8;  // C tile pitch in smem: conflict-free 16-byte fragment reads
+constexpr int STAGES = 3;                     // A/B ring depth
+// TMA boxes are 16 doubles (128 B, the SWIZZLE_128B span) wide:
+//   view 0: {16, 128} rows   k-contiguous A slices (2 boxes per BK = 32)
+//   view 1: {16, 64}  rows   k-contiguous B slices (2 boxes)
+//   view 2: {16, 32}  rows   m/n-contiguous slices, 32 k-rows (8 boxes for A, 4 for B)
+constexpr int NVIEW = 3;
+constexpr int A_STAGE_BYTES = BM * BK * 8, B_STAGE_BYTES = BN * BK * 8;
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int CS_LD = BN + 8;  // C tile pitch in smem (bulk row copies)
 constexpr int C_ELEMS = BM * CS_LD;
-constexpr int GEMM_SMEM_DOUBLES = STAGES * (A_ELEMS + B_ELEMS) + C_ELEMS;
+constexpr int GEMM_SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_ELEMS * 8;  // + 1024 alignment slack
+constexpr int GEMM_SMEM_DOUBLES = GEMM_SMEM_BYTES / 8;
 constexpr int TRI_LD = PB + 1;                // padded pitch of a bw x bw triangle in smem
 constexpr int TRI_SMEM_DOUBLES = PB * TRI_LD;
 
+// A matrix of a workspace slot: raw pointer + leading dimension, and its TMA descriptors
+// (NVIEW box shapes, see above; the tensor extent is the matrix allocation, out-of-range
+// boxes are zero filled).
+struct MatView {
+  const CUtensorMap *tm;
+  double *base;
+  int64_t ld;
+  __device__ __forceinline__ double *at(int r, int c) const {
+    return base + static_cast<int64_t>(r) * ld + c;
+  }
+};
+// An operand: the submatrix of `v` starting at (r0, c0). kc: element (i, k) of the operand is
+// v(r0 + i, c0 + k) (k contiguous); otherwise v(r0 + k, c0 + i).
+struct Op {
+  MatView v;
+  int r0, c0;
+  bool kc;
+};
+__device__ __forceinline__ Op opk(const MatView &v, int r0, int c0) { return Op{v, r0, c0, true}; }
+__device__ __forceinline__ Op opn(const MatView &v, int r0, int c0) { return Op{v, r0, c0, false}; }
+
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
-
-// Epilogues. kReadC: the accumulator starts from C (staged into shared memory by bulk async
-// copies, one tile ahead of its use); init() maps a C value to the initial accumulator and store2
-// writes the final pair (col, col+1) with the valid masks v0/v1 (r < M && c < N).
-struct EpiSub {  // C -= A.B   (acc = -C ; acc += A.B ; C = -acc : exact sign flips)
-  static constexpr bool kReadC = true;
-  double *C;
-  int64_t ldc;
-  __device__ __forceinline__ double init(double c) const { return -c; }
-  __device__ __forceinline__ void store2(int r, int c, bool v0, bool v1, double a0, double a1) const {
-    double *p = C + static_cast<int64_t>(r) * ldc + c;
-    if (v0) p[0] = -a0;
-    if (v1) p[1] = -a1;
-  }
-};
-
-struct EpiStore;
-__device__ __forceinline__ double epi_diag(const struct EpiSub &) { return 0.0; }
-__device__ __forceinline__ double epi_diag(const EpiStore &e);
-struct EpiStore {  // C = A.B + diag_add * I
-  static constexpr bool kReadC = false;
-  double *C;
-  int64_t ldc;
-  double diag_add;
-  __device__ __forceinline__ double init(double) const { return 0.0; }
-  __device__ __forceinline__ void store2(int r, int c, bool v0, bool v1, double a0, double a1) const {
-    double *p = C + static_cast<int64_t>(r) * ldc + c;
-    if (v0) p[0] = a0 + (r == c ? diag_add : 0.0);
-    if (v1) p[1] = a1 + (r == c + 1 ? diag_add : 0.0);
-  }
-};
-
-__device__ __forceinline__ double epi_diag(const EpiStore &e) { return e.diag_add; }
 
 // mbarriers of the gemm pipeline (re-initialised at every gemm call).
 struct GemmSync {
   uint64_t full[STAGES], empty[STAGES], cfull, cempty;
 };
-__device__ __forceinline__ void gemm_sync_init(GemmSync *) {}
 
 // Tile enumeration (row-major over tm); lower = only tiles holding some element with row >= col.
 __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
@@ -88,43 +76,38 @@ __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
 }
 
 __device__ __forceinline__ uint32_t round16(int bytes) { return static_cast<uint32_t>((bytes + 15) & ~15); }
+__device__ __forceinline__ int frag_perm(int g) { return (g >> 1) + 4 * (g & 1); }
 
-// Producer-warp helper: copy `nrows` rows of `rbytes` bytes (16-byte multiple) from
-// G + r*ld (r < nrows) to smem rows of pitch `ld_s` doubles; completion on bar.
+// Producer-warp helper: bulk-copy `nrows` rows of `rbytes` bytes (16-byte multiple) from
+// G + r*ld to smem rows of pitch `ld_s` doubles; completion on bar.
 __device__ __forceinline__ void bulk_rows(double *s, int ld_s, const double *G, int64_t ld,
                                           int nrows, uint32_t rbytes, uint64_t *bar) {
   for (int r = lane_id(); r < nrows; r += 32)
     bulk_g2s(smem_u32(s + r * ld_s), G + static_cast<int64_t>(r) * ld, rbytes, bar);
 }
 
-// C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).
-//   A_KC: A element (m, k) at A[m*lda + k], else at A[k*lda + m]; likewise B_KC for (n, k).
-//   All of A, B (and C if the epilogue reads it) must be 16-byte aligned with even leading
-//   dimensions; tiles are moved by cp.async.bulk (rows of a tile rounded up to 16 bytes, so up
-//   to 8 bytes past a row end may be read: callers' buffers are padded).
-// Warp-specialised pipeline without CTA-wide barriers in the main loop: warp NCW (producer) streams
-// BK-deep A/B slices into a STAGES ring and each tile's C into a single C buffer (prefetched
-// while the previous tile is still computing); warps 0..NCW-1 run FP64 DMMA on 32x32 warp tiles
-// and store their part of the tile directly to global memory.
 struct GemmArgs {
-  const double *A, *B;
-  double *C;
-  int64_t lda, ldb, ldc;
+  Op a, b;
+  double *C;      // C element (i, j) at C[i*ldc + j]
+  int64_t ldc;
   int M, N, K;
-  bool a_kc, b_kc, lower, read_c;  // read_c: C -= A.B (else C = A.B + diag_add I)
+  bool lower, read_c;  // read_c: C -= A.B (C must be 16-byte aligned, ldc even); else C = A.B + diag_add I
   double diag_add;
 };
 
-static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, GemmSync *gs) {
-  const double *A = ga.A, *B = ga.B;
-  const int64_t lda = ga.lda, ldb = ga.ldb;
+// C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).
+// Warp-specialised, no CTA-wide barrier in the main loop: warp NCW streams BK-deep A/B slices with
+// 2D TMA (SWIZZLE_128B boxes of the slot's tensor maps) into a STAGES-deep mbarrier ring, and each
+// tile's C (C -= A.B) into a C buffer by bulk row copies one tile ahead; warps 0..NCW-1 run FP64
+// DMMA on 32x32 warp tiles and store their part of the tile straight to global memory.
+// k-contiguous fragments are read as 16-byte (k, k+1) pairs; within each 8-row group fragment row
+// g maps to smem row (g>>1) + 4(g&1) so those reads are bank-conflict free under the swizzle.
+// Partial k-slices are masked (both operands zeroed beyond K).
+static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al, GemmSync *gs) {
   const int M = ga.M, N = ga.N, K = ga.K;
-  const bool A_KC = ga.a_kc, B_KC = ga.b_kc, lower = ga.lower, readC = ga.read_c;
+  const bool A_KC = ga.a.kc, B_KC = ga.b.kc, lower = ga.lower, readC = ga.read_c;
   __syncthreads();
-  if (M <= 0 || N <= 0 || K <= 0) {
-    // K == 0 only ever comes with EpiStore(0) in this library: nothing to accumulate
-    return;
-  }
+  if (M <= 0 || N <= 0 || K <= 0) return;  // K == 0 only comes with C = 0 * ... never used
   if (threadIdx.x == 0) {
     for (int st = 0; st < STAGES; ++st) {
       mbar_init(&gs->full[st], 1);
@@ -140,9 +123,7 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
   int ntiles = 0;
   for (int tm = 0; tm < tiles_m; ++tm) ntiles += tiles_in_row(tm, tiles_n, lower);
   const int total = ntiles * nkc;
-  double *Cs = smem + STAGES * (A_ELEMS + B_ELEMS);
-  auto As = [&](int st) { return smem + st * (A_ELEMS + B_ELEMS); };
-  auto Bs = [&](int st) { return smem + st * (A_ELEMS + B_ELEMS) + A_ELEMS; };
+  double *Cs = reinterpret_cast<double *>(smem_al + STAGES * STAGE_BYTES);
   auto decode_tile = [&](int tile, int &tm, int &tn) {
     tm = 0;
     int cnt;
@@ -157,8 +138,14 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
   if (warp == NCW) {
     // ============================ producer warp ============================
     // generic-proxy global writes of earlier phases (made CTA-visible by the barrier above) must be
-    // ordered before this warp's async-proxy bulk reads
+    // ordered before the async-proxy (TMA / bulk) reads issued below
     asm volatile("fence.proxy.async;\n" ::: "memory");
+    const CUtensorMap *tmA = ga.a.v.tm + (A_KC ? 0 : 2);
+    const CUtensorMap *tmB = ga.b.v.tm + (B_KC ? 1 : 2);
+    if (lane == 0) {
+      tma_prefetch_desc(tmA);
+      tma_prefetch_desc(tmB);
+    }
     for (int it = 0; it < total; ++it) {
       const int st = it % STAGES, use = it / STAGES;
       const int tile = it / nkc, kc = it % nkc;
@@ -174,31 +161,41 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
                   rb, &gs->cfull);
       }
       if (it >= STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
-      const int k0 = kc * BK, krem = min(BK, K - k0);
-      const int ra = min(BM, M - tm * BM), rbn = min(BN, N - tn * BN);
-      const uint32_t a_rb = A_KC ? round16(krem * 8) : round16(ra * 8);
-      const int a_nr = A_KC ? ra : krem;
-      const uint32_t b_rb = B_KC ? round16(krem * 8) : round16(rbn * 8);
-      const int b_nr = B_KC ? rbn : krem;
-      if (lane == 0) mbar_arrive_expect_tx(&gs->full[st], a_rb * a_nr + b_rb * b_nr);
+      if (lane == 0) {
+        const int k0 = kc * BK;
+        uint64_t *bar = &gs->full[st];
+        mbar_arrive_expect_tx(bar, STAGE_BYTES);
+        const uint32_t sa = smem_u32(smem_al + st * STAGE_BYTES), sb = sa + A_STAGE_BYTES;
+        if (A_KC) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            tma_load_2d(sa + q * (BM * 128), tmA, bar, ga.a.c0 + k0 + 16 * q, ga.a.r0 + tm * BM);
+        } else {
+#pragma unroll
+          for (int q = 0; q < BM / 16; ++q)
+            tma_load_2d(sa + q * (BK * 128), tmA, bar, ga.a.c0 + tm * BM + 16 * q, ga.a.r0 + k0);
+        }
+        if (B_KC) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            tma_load_2d(sb + q * (BN * 128), tmB, bar, ga.b.c0 + k0 + 16 * q, ga.b.r0 + tn * BN);
+        } else {
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q)
+            tma_load_2d(sb + q * (BK * 128), tmB, bar, ga.b.c0 + tn * BN + 16 * q, ga.b.r0 + k0);
+        }
+      }
       __syncwarp();
-      if (A_KC)
-        bulk_rows(As(st), KC_LD, A + static_cast<int64_t>(tm * BM) * lda + k0, lda, a_nr, a_rb,
-                  &gs->full[st]);
-      else
-        bulk_rows(As(st), A_MC_LD, A + static_cast<int64_t>(k0) * lda + tm * BM, lda, a_nr, a_rb,
-                  &gs->full[st]);
-      if (B_KC)
-        bulk_rows(Bs(st), KC_LD, B + static_cast<int64_t>(tn * BN) * ldb + k0, ldb, b_nr, b_rb,
-                  &gs->full[st]);
-      else
-        bulk_rows(Bs(st), B_NC_LD, B + static_cast<int64_t>(k0) * ldb + tn * BN, ldb, b_nr, b_rb,
-                  &gs->full[st]);
     }
   } else {
     // ============================ consumer warps ============================
     const int wm = warp % WM, wn = warp / WM;
     const int g = lane >> 2, t = lane & 3;
+    const int pg = frag_perm(g);
+    const int arow = A_KC ? pg : g;  // smem row / m offset of this lane's A fragment rows
+    // local (row, col) of acc[mi][ni][h] inside the tile
+    auto acc_row = [&](int mi) { return wm * WTM + mi * 8 + arow; };
+    auto acc_col = [&](int ni, int h) { return wn * WTN + ni * 8 + (B_KC ? t + 4 * h : 2 * t + h); };
     double acc[MI][NI][2];
     for (int it = 0; it < total; ++it) {
       const int st = it % STAGES, use = it / STAGES;
@@ -212,10 +209,9 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
           for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
-              double c0, c1;
-              lds128(c0, c1, smem_u32(Cs + (wm * WTM + mi * 8 + g) * CS_LD + wn * WTN + ni * 8 + 2 * t));
-              acc[mi][ni][0] = -c0;  // C -= A.B as acc = -C; acc += A.B; C = -acc (exact)
-              acc[mi][ni][1] = -c1;
+              const double *cr = Cs + acc_row(mi) * CS_LD;
+              acc[mi][ni][0] = -cr[acc_col(ni, 0)];  // C -= A.B as acc = -C; acc += A.B; C = -acc
+              acc[mi][ni][1] = -cr[acc_col(ni, 1)];
             }
           __syncwarp();
           if (lane == 0) mbar_arrive(&gs->cempty);
@@ -228,7 +224,7 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
       }
       mbar_wait(&gs->full[st], use & 1);
       const int krem = min(BK, K - kc * BK);
-      const double *as = As(st), *bs = Bs(st);
+      const uint32_t sa = smem_u32(smem_al + st * STAGE_BYTES), sb = sa + A_STAGE_BYTES;
 #pragma unroll 1
       for (int k8 = 0; k8 < BK / 8; ++k8) {
         if (k8 * 8 >= krem) break;
@@ -236,25 +232,33 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
         double a[MI][2], b[NI][2];
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
-          const int m = wm * WTM + mi * 8 + g;
           if (A_KC) {
-            lds128(a[mi][0], a[mi][1], smem_u32(as + m * KC_LD + k));
+            const int r = wm * WTM + mi * 8 + pg;  // r & 7 == pg
+            const uint32_t chunk = static_cast<uint32_t>((((k8 & 1) * 4 + t) ^ pg) << 4);
+            lds128(a[mi][0], a[mi][1], sa + (k8 >> 1) * (BM * 128) + r * 128 + chunk);
           } else {
-            a[mi][0] = as[k * A_MC_LD + m];
-            a[mi][1] = as[(k + 1) * A_MC_LD + m];
+            const int m = wm * WTM + mi * 8 + g;
+            const uint32_t base = sa + (m >> 4) * (BK * 128) + ((m & 1) << 3);
+            const int j2 = (m & 15) >> 1;
+            a[mi][0] = lds64(base + k * 128 + ((j2 ^ (k & 7)) << 4));
+            a[mi][1] = lds64(base + (k + 1) * 128 + ((j2 ^ ((k + 1) & 7)) << 4));
           }
         }
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) {
-          const int n = wn * WTN + ni * 8 + g;
           if (B_KC) {
-            lds128(b[ni][0], b[ni][1], smem_u32(bs + n * KC_LD + k));
+            const int r = wn * WTN + ni * 8 + pg;
+            const uint32_t chunk = static_cast<uint32_t>((((k8 & 1) * 4 + t) ^ pg) << 4);
+            lds128(b[ni][0], b[ni][1], sb + (k8 >> 1) * (BN * 128) + r * 128 + chunk);
           } else {
-            b[ni][0] = bs[k * B_NC_LD + n];
-            b[ni][1] = bs[(k + 1) * B_NC_LD + n];
+            const int n = wn * WTN + ni * 8 + g;
+            const uint32_t base = sb + (n >> 4) * (BK * 128) + ((n & 1) << 3);
+            const int j2 = (n & 15) >> 1;
+            b[ni][0] = lds64(base + k * 128 + ((j2 ^ (k & 7)) << 4));
+            b[ni][1] = lds64(base + (k + 1) * 128 + ((j2 ^ ((k + 1) & 7)) << 4));
           }
         }
-        if (k8 * 8 + 8 > krem) {  // partial slice: zero both operands beyond K (stale smem)
+        if (k8 * 8 + 8 > krem) {  // partial slice: zero both operands beyond K
           const bool v0 = k < krem, v1 = k + 1 < krem;
 #pragma unroll
           for (int mi = 0; mi < MI; ++mi) {
@@ -280,20 +284,20 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
       if (kc == nkc - 1) {
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
-          const int r = tm * BM + wm * WTM + mi * 8 + g;
+          const int r = tm * BM + acc_row(mi);
+          if (r >= M) continue;
+          double *crow = ga.C + static_cast<int64_t>(r) * ga.ldc;
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni) {
-            const int c = tn * BN + wn * WTN + ni * 8 + 2 * t;
-            const bool v0 = r < M && c < N, v1 = r < M && c + 1 < N;
-            double *p = ga.C + static_cast<int64_t>(r) * ga.ldc + c;
-            if (readC) {
-              if (v0) p[0] = -acc[mi][ni][0];
-              if (v1) p[1] = -acc[mi][ni][1];
-            } else {
-              if (v0) p[0] = acc[mi][ni][0] + (r == c ? ga.diag_add : 0.0);
-              if (v1) p[1] = acc[mi][ni][1] + (r == c + 1 ? ga.diag_add : 0.0);
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = tn * BN + acc_col(ni, h);
+              if (c >= N) continue;
+              if (readC)
+                crow[c] = -acc[mi][ni][h];
+              else
+                crow[c] = acc[mi][ni][h] + (r == c ? ga.diag_add : 0.0);
             }
-          }
         }
       }
     }
@@ -301,27 +305,24 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, double *smem, Ge
   __syncthreads();
 }
 
-// Typed front end: builds the runtime argument block (one compiled instance of the pipeline).
-template <bool A_KC, bool B_KC, class Epi>
-__device__ __forceinline__ void gemm(int M, int N, int K, const double *A, int64_t lda, const double *B,
-                                     int64_t ldb, bool lower, double *smem, GemmSync *gs,
-                                     const Epi &epi) {
-  GemmArgs ga;
-  ga.A = A;
-  ga.B = B;
-  ga.C = epi.C;
-  ga.lda = lda;
-  ga.ldb = ldb;
-  ga.ldc = epi.ldc;
-  ga.M = M;
-  ga.N = N;
-  ga.K = K;
-  ga.a_kc = A_KC;
-  ga.b_kc = B_KC;
-  ga.lower = lower;
-  ga.read_c = Epi::kReadC;
-  ga.diag_add = Epi::kReadC ? 0.0 : epi_diag(epi);
-  gemm_rt(ga, smem, gs);
+// Front ends (one compiled instance of the pipeline for every call site).
+__device__ __forceinline__ uint8_t *gemm_smem_align(double *smem) {
+  return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 1023) &
+                                     ~static_cast<uintptr_t>(1023));
+}
+// C -= A.B   (C = the submatrix of `c` at (r0, c0))
+__device__ __forceinline__ void gemm_sub(int M, int N, int K, const Op &a, const Op &b,
+                                         const MatView &c, int cr0, int cc0, bool lower,
+                                         double *smem, GemmSync *gs) {
+  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, true, 0.0};
+  gemm_rt(ga, gemm_smem_align(smem), gs);
+}
+// C = A.B + diag_add I
+__device__ __forceinline__ void gemm_set(int M, int N, int K, const Op &a, const Op &b,
+                                         const MatView &c, int cr0, int cc0, bool lower,
+                                         double diag_add, double *smem, GemmSync *gs) {
+  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, diag_add};
+  gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 
 // ------------------------------------------------------------------------------------------------

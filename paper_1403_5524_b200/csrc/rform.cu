@@ -281,6 +281,27 @@ static PFN_encodeTiled_t get_encode_fn() {
   return fn;
 }
 
+bool encode_tmap_f64(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows, std::string &err) {
+  PFN_encodeTiled_t enc = get_encode_fn();
+  if (!enc) {
+    err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) + ")";
+    return false;
+  }
+  return true;
+}
+
 template <class C>
 static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *Ek, int nch,
                                     int nlev, double a, const double *E, int64_t ne, double *R,

@@ -25,6 +25,10 @@ struct rmx_ctx {
   // linear-algebra workspace (match / tepi slots)
   double *ws = nullptr;
   size_t ws_bytes = 0;
+  // TMA descriptor tables of the workspace slots (device memory), rebuilt when ws / nch change
+  CUtensorMap *match_views = nullptr, *tepi_views = nullptr;
+  int64_t views_nch = -1, views_slots = -1;
+  const double *views_ws = nullptr;
   // sweep batch buffer (R, then K in place)
   double *rbuf = nullptr;
   size_t rbuf_bytes = 0;
@@ -119,14 +123,59 @@ rmx_rc grow(rmx_ctx *c, void **p, size_t *have, size_t need) {
 
 rmx_rc grow(rmx_ctx *c, rmx_ctx::Dev &d, size_t need) { return grow(c, &d.p, &d.bytes, need); }
 
+// One CTA per SM (the per-energy kernels use ~220 KB of shared memory): slots = #SMs.
 int64_t ws_slots_for(const rmx_ctx *c, int64_t ne) {
-  return std::min<int64_t>(ne, 2 * static_cast<int64_t>(c->nsm));
+  return std::min<int64_t>(ne, static_cast<int64_t>(c->nsm));
 }
 
+rmx_rc build_views(rmx_ctx *c, CUtensorMap **dst, int64_t nch, int64_t slots, int64_t per_slot,
+                   const std::vector<MatSpec> &specs) {
+  const int nview = 3;
+  std::vector<CUtensorMap> h(static_cast<size_t>(slots * specs.size() * nview));
+  std::string err;
+  for (int64_t s = 0; s < slots; ++s)
+    for (size_t m = 0; m < specs.size(); ++m)
+      for (int v = 0; v < nview; ++v) {
+        const MatSpec &sp = specs[m];
+        const double *base = c->ws + s * per_slot + sp.off;
+        if (!encode_tmap_f64(&h[(s * specs.size() + m) * nview + v], base, sp.rows, sp.cols, sp.ld,
+                             kViewBoxRows[v], err))
+          return fail(c, RMX_ECUDA, "tensor map: " + err);
+      }
+  if (*dst) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(*dst);
+    *dst = nullptr;
+  }
+  cudaError_t e = cudaMalloc(dst, h.size() * sizeof(CUtensorMap));
+  if (e != cudaSuccess) return fail(c, RMX_ENOMEM, "cudaMalloc(tensor maps) failed");
+  e = cudaMemcpy(*dst, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(c, e, "tensor map upload");
+  return RMX_OK;
+}
+
+int64_t ws_slot_doubles(int64_t nch) {
+  return std::max(match_ws_doubles_per_slot(nch), tepi_ws_doubles_per_slot(nch));
+}
+
+// Workspace for `slots` per-energy slots of the matching / T kernels, with their TMA views.
 rmx_rc ensure_ws(rmx_ctx *c, int64_t nch, int64_t slots) {
-  const int64_t per = std::max(match_ws_doubles_per_slot(nch), tepi_ws_doubles_per_slot(nch));
-  return grow(c, reinterpret_cast<void **>(&c->ws), &c->ws_bytes,
-              static_cast<size_t>(per * slots) * sizeof(double));
+  slots = std::max<int64_t>(slots, c->views_slots);  // never shrink below what views cover
+  const int64_t per = ws_slot_doubles(nch);
+  rmx_rc rc = grow(c, reinterpret_cast<void **>(&c->ws), &c->ws_bytes,
+                   static_cast<size_t>(per * slots) * sizeof(double) + 4096);
+  if (rc != RMX_OK) return rc;
+  if (c->views_ws != c->ws || c->views_nch != nch || c->views_slots < slots) {
+    std::vector<MatSpec> specs;
+    match_view_specs(nch, specs);
+    if ((rc = build_views(c, &c->match_views, nch, slots, per, specs)) != RMX_OK) return rc;
+    tepi_view_specs(nch, specs);
+    if ((rc = build_views(c, &c->tepi_views, nch, slots, per, specs)) != RMX_OK) return rc;
+    c->views_ws = c->ws;
+    c->views_nch = nch;
+    c->views_slots = slots;
+  }
+  return RMX_OK;
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -168,6 +217,8 @@ rmx_rc rmx_destroy(rmx_ctx *c) {
   for (auto e : c->free_events) cudaEventDestroy(e);
   cudaFree(c->ws);
   cudaFree(c->rbuf);
+  cudaFree(c->match_views);
+  cudaFree(c->tepi_views);
   for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
                   &c->dst})
     cudaFree(d->p);
@@ -220,7 +271,8 @@ rmx_rc rmx_match_K(rmx_ctx *c, const double *R, const double *F, const double *G
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   cudaError_t e = timed(c, RMX_KID_MATCH, 1, [&] {
-    return launch_match(R, F, G, Fp, Gp, a, nch, ne, n_open, K, c->ws, slots, status, c->stream);
+    return launch_match(R, F, G, Fp, Gp, a, nch, ne, n_open, K, c->ws, ws_slot_doubles(nch), c->match_views, slots, status,
+                        c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_match_K");
   return RMX_OK;
@@ -239,8 +291,8 @@ rmx_rc rmx_collision_strength(rmx_ctx *c, const double *K, int64_t nch, int64_t 
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
-    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, c->ws, slots,
-                       status, c->stream);
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, c->ws, ws_slot_doubles(nch), c->tepi_views,
+                       slots, status, c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_collision_strength");
   return RMX_OK;
@@ -297,7 +349,7 @@ rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int
                         cudaMemcpyDeviceToDevice, c->stream);
     e = timed(c, RMX_KID_MATCH, 1, [&] {
       return launch_match(rb, F + b0 * nch, G + b0 * nch, Fp + b0 * nch, Gp + b0 * nch, a, nch, nb,
-                          nob, rb, c->ws, slots, stb, c->stream);
+                          nob, rb, c->ws, ws_slot_doubles(nch), c->match_views, slots, stb, c->stream);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/K");
     for (int64_t d = 0; d < n_dump; ++d) {
@@ -309,14 +361,14 @@ rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int
       if (T2_d) {
         e = timed(c, RMX_KID_TEPI, 1, [&] {
           return launch_tepi(rb + l * mat, nch, mat, nch, 1, nob ? nob + l : nullptr, T2_d + d * mat,
-                             nullptr, nullptr, c->ws, 1, nullptr, c->stream);
+                             nullptr, nullptr, c->ws, ws_slot_doubles(nch), c->tepi_views, 1, nullptr, c->stream);
         });
         if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T dump");
       }
     }
     e = timed(c, RMX_KID_TEPI, 1, [&] {
       return launch_tepi(rb, nch, mat, nch, nb, nob, nullptr, nullptr, rowsum + b0 * nch, c->ws,
-                         slots, stb, c->stream);
+                         ws_slot_doubles(nch), c->tepi_views, slots, stb, c->stream);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T");
   }

@@ -32,6 +32,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double x;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(x) : "r"(addr));
+  return x;
+}
 __device__ __forceinline__ void lds128(double &x, double &y, uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
 }

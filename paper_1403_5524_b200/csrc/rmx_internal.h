@@ -2,28 +2,74 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "../../include/rmx.h"
 
 namespace rmx {
+
+// A matrix inside one workspace slot that the per-energy kernels read with TMA:
+// offset (doubles from the slot start), rows, tensor width (columns), leading dimension.
+struct MatSpec {
+  int64_t off, rows, cols, ld;
+};
+
+// Per-slot workspace layouts (doubles) of the matching and T kernels; every matrix start is
+// 16-byte aligned and followed by 32 doubles of padding (bulk copies round rows up to 16 bytes).
+struct MatchLayout {
+  int64_t npad, ldm, m_off, tg_off, slot;
+};
+struct TepiLayout {
+  int64_t ldo, s_off, x_off, k_off, tg_off, slot;
+};
+__host__ __device__ inline MatchLayout match_layout(int64_t nch) {
+  MatchLayout L;
+  L.npad = (nch + 1) & ~1LL;
+  L.ldm = 2 * L.npad;  // [A | pad | B_open]
+  L.m_off = 0;
+  L.tg_off = nch * L.ldm + 32;
+  L.slot = L.tg_off + 32 * 32 + 32;
+  return L;
+}
+__host__ __device__ inline TepiLayout tepi_layout(int64_t nch) {
+  TepiLayout L;
+  L.ldo = (nch + 1) & ~1LL;
+  L.s_off = 0;
+  L.x_off = nch * L.ldo + 32;
+  L.k_off = L.x_off + nch * L.ldo + 32;
+  L.tg_off = L.k_off + nch * L.ldo + 32;
+  L.slot = L.tg_off + 32 * 32 + 32;
+  return L;
+}
 
 // rform.cu
 int rform_tile_for(int64_t nch);
 cudaError_t launch_rform(const double *w, int64_t ldw, const double *Ek, int64_t nch, int64_t nlev,
                          double a, const double *E, int64_t ne, double *R, int32_t *status,
                          cudaStream_t st, std::string &err);
+// host helper shared with the view tables: encode a 2D FP64 tensor map (box {16, box_rows},
+// SWIZZLE_128B, zero fill out of range)
+bool encode_tmap_f64(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows, std::string &err);
 
 // match.cu
-size_t match_smem_bytes();
 int64_t match_ws_doubles_per_slot(int64_t nch);
+void match_view_specs(int64_t nch, std::vector<MatSpec> &specs);
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,
                          const double *Gp, double a, int64_t nch, int64_t ne, const int32_t *n_open,
-                         double *K, double *ws, int64_t ws_slots, int32_t *status, cudaStream_t st);
+                         double *K, double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
+                         int32_t *status, cudaStream_t st);
 
 // tepi.cu
 int64_t tepi_ws_doubles_per_slot(int64_t nch);
+void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs);
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
-                        double *ws, int64_t ws_slots, int32_t *status, cudaStream_t st);
+                        double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
+                        int32_t *status, cudaStream_t st);
+
+// box rows of the NVIEW tensor-map variants used by the CTA GEMM (cta_la.cuh)
+constexpr int kViewBoxRows[3] = {128, 64, 32};
 
 }  // namespace rmx

@@ -14,26 +14,36 @@ namespace rmx {
 using namespace la;
 
 struct TepiSmem {
-  double gemm[GEMM_SMEM_DOUBLES];
-  double tri[TRI_SMEM_DOUBLES];
+  union {  // the triangle scratch is only used between gemm calls
+    double gemm[GEMM_SMEM_DOUBLES];
+    double tri[TRI_SMEM_DOUBLES];
+  };
   GemmSync gs;
 };
 
+
+// Workspace slot: S (then P) [o][ldo], X [o][ldo], Kc [o][ldo] (aligned copy of K_oo),
+// Tg [32][32] (inverse of a 32x32 diagonal block of L: triangular solves run as DMMA GEMMs).
 // Factorisation / solves use outer blocks of NB = 64 (two inner 32-wide triangles) so that the
 // big updates run with K = 64.
 __global__ void __launch_bounds__(NT, 1)
     tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
                 const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
-                double *rowsum, double *ws, int64_t ws_slot, int ldo, int32_t *status) {
+                double *rowsum, double *ws, int64_t ws_slot, const CUtensorMap *views,
+                int32_t *status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TepiSmem &sm = *reinterpret_cast<TepiSmem *>(smem_raw);
-  gemm_sync_init(&sm.gs);
-  double *S = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;  // o x ldo; later holds P
-  double *X = S + static_cast<int64_t>(n) * ldo;                // o x ldo
-  double *Kc = X + static_cast<int64_t>(n) * ldo;               // o x ldo: aligned copy of K_oo
-  double *Tg = Kc + static_cast<int64_t>(n) * ldo + 32;          // PB x PB diagonal-block inverse
-  auto Sp = [&](int r, int c) { return S + static_cast<int64_t>(r) * ldo + c; };
-  auto Xr = [&](int r) { return X + static_cast<int64_t>(r) * ldo; };
+  const TepiLayout L = tepi_layout(n);
+  const int ldo = static_cast<int>(L.ldo);
+  double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
+  const CUtensorMap *vw = views + blockIdx.x * 4 * NVIEW;
+  const MatView Sv{vw + 0 * NVIEW, slot + L.s_off, ldo};
+  const MatView Xv{vw + 1 * NVIEW, slot + L.x_off, ldo};
+  const MatView Kv{vw + 2 * NVIEW, slot + L.k_off, ldo};
+  const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, PB};
+  double *S = Sv.base, *Tg = Tv.base;
+  double *smg = sm.gemm;
+  GemmSync *gs = &sm.gs;
 
   for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
     int o = n_open ? n_open[e] : n;
@@ -41,82 +51,76 @@ __global__ void __launch_bounds__(NT, 1)
     const double *Ke = K + e * kstride;
     double *T2e = nullptr;
     if (T2) {
-      const int64_t slot = t2_slot ? t2_slot[e] : e;
-      if (slot >= 0) T2e = T2 + slot * static_cast<int64_t>(n) * n;
+      const int64_t ts = t2_slot ? t2_slot[e] : e;
+      if (ts >= 0) T2e = T2 + ts * static_cast<int64_t>(n) * n;
     }
     int bad = 0;
     if (o > 0) {
-      // Kc = X = K_oo (16-byte aligned, even pitch: operands of the bulk-copy GEMM pipeline)
+      // Kc = X = K_oo (aligned, even pitch: operands of the TMA GEMM pipeline)
       for (int i = warp_id(); i < o; i += NW)
         for (int j = lane_id(); j < o; j += 32) {
           const double v = Ke[static_cast<int64_t>(i) * ldk + j];
-          Kc[static_cast<int64_t>(i) * ldo + j] = v;
-          Xr(i)[j] = v;
+          *Kv.at(i, j) = v;
+          *Xv.at(i, j) = v;
         }
       __syncthreads();
       // S = I + K_oo K_oo^T (lower tiles)
-      gemm<true, true>(o, o, o, Kc, ldo, Kc, ldo, true, sm.gemm, &sm.gs, EpiStore{S, ldo, 1.0});
+      gemm_set(o, o, o, opk(Kv, 0, 0), opk(Kv, 0, 0), Sv, 0, 0, true, 1.0, smg, gs);
       // blocked Cholesky S = L L^T (lower); panel solves L21 = S21 L11^{-T} as in-place GEMMs
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
         bad |= chol_diag(S, ldo, P0, w1, sm.tri);
         tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
         if (P0 + w1 < o)
-          gemm<true, true>(o - P0 - w1, w1, w1, Sp(P0 + w1, P0), ldo, Tg, PB, false, sm.gemm, &sm.gs,
-                           EpiStore{Sp(P0 + w1, P0), ldo, 0.0});
+          gemm_set(o - P0 - w1, w1, w1, opk(Sv, P0 + w1, P0), opk(Tv, 0, 0), Sv, P0 + w1, P0, false,
+                   0.0, smg, gs);
         if (w2 > 0) {
-          gemm<true, true>(o - P0 - w1, w2, w1, Sp(P0 + w1, P0), ldo, Sp(P0 + w1, P0), ldo, false,
-                           sm.gemm, &sm.gs, EpiSub{Sp(P0 + w1, P0 + w1), ldo});
+          gemm_sub(o - P0 - w1, w2, w1, opk(Sv, P0 + w1, P0), opk(Sv, P0 + w1, P0), Sv, P0 + w1,
+                   P0 + w1, false, smg, gs);
           bad |= chol_diag(S, ldo, P0 + w1, w2, sm.tri);
           if (P0 + W < o) {
             tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
-            gemm<true, true>(o - P0 - W, w2, w2, Sp(P0 + W, P0 + w1), ldo, Tg, PB, false, sm.gemm,
-                             &sm.gs, EpiStore{Sp(P0 + W, P0 + w1), ldo, 0.0});
+            gemm_set(o - P0 - W, w2, w2, opk(Sv, P0 + W, P0 + w1), opk(Tv, 0, 0), Sv, P0 + W, P0 + w1,
+                     false, 0.0, smg, gs);
           }
         }
         if (P0 + W < o) {
           const int m2 = o - P0 - W;
-          gemm<true, true>(m2, m2, W, Sp(P0 + W, P0), ldo, Sp(P0 + W, P0), ldo, true, sm.gemm, &sm.gs,
-                           EpiSub{Sp(P0 + W, P0 + W), ldo});
+          gemm_sub(m2, m2, W, opk(Sv, P0 + W, P0), opk(Sv, P0 + W, P0), Sv, P0 + W, P0 + W, true,
+                   smg, gs);
         }
       }
       // forward: L Z = K  (X holds K_oo)
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
         tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
-        gemm<true, false>(w1, o, w1, Tg, PB, Xr(P0), ldo, false, sm.gemm, &sm.gs, EpiStore{Xr(P0), ldo, 0.0});
+        gemm_set(w1, o, w1, opk(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
         if (w2 > 0) {
-          gemm<true, false>(w2, o, w1, Sp(P0 + w1, P0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
-                            EpiSub{Xr(P0 + w1), ldo});
+          gemm_sub(w2, o, w1, opk(Sv, P0 + w1, P0), opn(Xv, P0, 0), Xv, P0 + w1, 0, false, smg, gs);
           tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
-          gemm<true, false>(w2, o, w2, Tg, PB, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
-                            EpiStore{Xr(P0 + w1), ldo, 0.0});
+          gemm_set(w2, o, w2, opk(Tv, 0, 0), opn(Xv, P0 + w1, 0), Xv, P0 + w1, 0, false, 0.0, smg, gs);
         }
         if (P0 + W < o)
-          gemm<true, false>(o - P0 - W, o, W, Sp(P0 + W, P0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
-                            EpiSub{Xr(P0 + W), ldo});
+          gemm_sub(o - P0 - W, o, W, opk(Sv, P0 + W, P0), opn(Xv, P0, 0), Xv, P0 + W, 0, false, smg, gs);
       }
       // backward: L^T X = Z
       for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
         const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
         if (w2 > 0) {
           tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
-          // X_b = L_bb^{-T} X_b : A(m,k) = Tg[k][m] -> [K][M]
-          gemm<false, false>(w2, o, w2, Tg, PB, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
-                             EpiStore{Xr(P0 + w1), ldo, 0.0});
+          // X_b = L_bb^{-T} X_b : A(m,k) = Tg[k][m]
+          gemm_set(w2, o, w2, opn(Tv, 0, 0), opn(Xv, P0 + w1, 0), Xv, P0 + w1, 0, false, 0.0, smg, gs);
           // X_a -= (L[P0+w1:P0+W, P0:P0+w1])^T X_b
-          gemm<false, false>(w1, o, w2, Sp(P0 + w1, P0), ldo, Xr(P0 + w1), ldo, false, sm.gemm, &sm.gs,
-                             EpiSub{Xr(P0), ldo});
+          gemm_sub(w1, o, w2, opn(Sv, P0 + w1, P0), opn(Xv, P0 + w1, 0), Xv, P0, 0, false, smg, gs);
         }
         tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
-        gemm<false, false>(w1, o, w1, Tg, PB, Xr(P0), ldo, false, sm.gemm, &sm.gs, EpiStore{Xr(P0), ldo, 0.0});
+        gemm_set(w1, o, w1, opn(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
         if (P0 > 0)
-          // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]; A(i,k) = S[(P0+k)*ldo + i] -> [K][M]
-          gemm<false, false>(P0, o, W, Sp(P0, 0), ldo, Xr(P0), ldo, false, sm.gemm, &sm.gs,
-                             EpiSub{X, ldo});
+          // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]
+          gemm_sub(P0, o, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
       }
       // P = K_oo X  (into S's storage)
-      gemm<true, false>(o, o, o, Kc, ldo, X, ldo, false, sm.gemm, &sm.gs, EpiStore{S, ldo, 0.0});
+      gemm_set(o, o, o, opk(Kv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, false, 0.0, smg, gs);
     }
     // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
@@ -124,8 +128,8 @@ __global__ void __launch_bounds__(NT, 1)
       for (int j = lane_id(); j < n; j += 32) {
         double v = 0.0;
         if (i < o && j < o) {
-          const double x = Xr(i)[j];
-          const double p = *Sp(i, j);
+          const double x = *Xv.at(i, j);
+          const double p = *Sv.at(i, j);
           v = 4.0 * fma(x, x, p * p);
           if (!isfinite(v)) bad = 1;
         }
@@ -141,14 +145,19 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
-int64_t tepi_ws_doubles_per_slot(int64_t nch) {
-  const int64_t npad = (nch + 1) & ~1LL;
-  return 3 * nch * npad + 32 + 32 * 32 + 32;  // + tail padding for 16-byte bulk copies of odd-width C tiles
+int64_t tepi_ws_doubles_per_slot(int64_t nch) { return tepi_layout(nch).slot; }
+
+// Matrices of one slot whose TMA descriptors the kernel uses: (S, X, Kc, Tg), NVIEW boxes each.
+void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
+  const TepiLayout L = tepi_layout(nch);
+  specs = {MatSpec{L.s_off, nch, L.ldo, L.ldo}, MatSpec{L.x_off, nch, L.ldo, L.ldo},
+           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, 32, 32, 32}};
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
-                        double *ws, int64_t ws_slots, int32_t *status, cudaStream_t st) {
+                        double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
+                        int32_t *status, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t ce = cudaFuncSetAttribute(tepi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -156,12 +165,9 @@ cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t n
     if (ce != cudaSuccess) return ce;
     attr = true;
   }
-  const int64_t npad = (nch + 1) & ~1LL;
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
   tepi_kernel<<<grid, NT, sizeof(TepiSmem), st>>>(K, ldk, kstride, static_cast<int>(nch), ne, n_open,
-                                                  T2, t2_slot, rowsum, ws,
-                                                  tepi_ws_doubles_per_slot(nch),
-                                                  static_cast<int>(npad), status);
+                                                  T2, t2_slot, rowsum, ws, ws_slot, views, status);
   return cudaGetLastError();
 }
 
