@@ -38,7 +38,9 @@ constexpr int C_ELEMS = BM * CS_LD;
 constexpr int GEMM_SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_ELEMS * 8;  // + 1024 alignment slack
 constexpr int GEMM_SMEM_DOUBLES = GEMM_SMEM_BYTES / 8;
 constexpr int TRI_LD = PB + 1;                // padded pitch of a bw x bw triangle in smem
-constexpr int TRI_SMEM_DOUBLES = PB * TRI_LD;
+constexpr int TB = NB;                        // edge of the diagonal-block inverses (64)
+constexpr int TB_LD = TB + 1;
+constexpr int TRI_SMEM_DOUBLES = 2 * TB * TB_LD;  // block + its inverse (aliases the gemm smem)
 
 // A matrix of a workspace slot: raw pointer + leading dimension, and its TMA descriptors
 // (NVIEW box shapes, see above; the tensor extent is the matrix allocation, out-of-range
@@ -88,10 +90,11 @@ __device__ __forceinline__ void bulk_rows(double *s, int ld_s, const double *G, 
 
 struct GemmArgs {
   Op a, b;
-  double *C;      // C element (i, j) at C[i*ldc + j]
+  double *C;      // C element (i, j) at C[i*ldc + j]   (trans_c: at C[j*ldc + i])
   int64_t ldc;
   int M, N, K;
   bool lower, read_c;  // read_c: C -= A.B (C must be 16-byte aligned, ldc even); else C = A.B + diag_add I
+  bool trans_c;        // store the result transposed (only with read_c == false)
   double diag_add;
 };
 
@@ -271,13 +274,13 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al
             b[ni][1] = v1 ? b[ni][1] : 0.0;
           }
         }
+        // k-slot 0 for all 16 accumulators, then k-slot 1: dependent DMMAs are 16 issues apart
 #pragma unroll
-        for (int mi = 0; mi < MI; ++mi)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni) {
-            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][0], b[ni][0]);
-            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][1], b[ni][1]);
-          }
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][h], b[ni][h]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs->empty[st]);
@@ -295,6 +298,8 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al
               if (c >= N) continue;
               if (readC)
                 crow[c] = -acc[mi][ni][h];
+              else if (ga.trans_c)
+                ga.C[static_cast<int64_t>(c) * ga.ldc + r] = acc[mi][ni][h];
               else
                 crow[c] = acc[mi][ni][h] + (r == c ? ga.diag_add : 0.0);
             }
@@ -314,14 +319,23 @@ __device__ __forceinline__ uint8_t *gemm_smem_align(double *smem) {
 __device__ __forceinline__ void gemm_sub(int M, int N, int K, const Op &a, const Op &b,
                                          const MatView &c, int cr0, int cc0, bool lower,
                                          double *smem, GemmSync *gs) {
-  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, true, 0.0};
+  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, true, false, 0.0};
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 // C = A.B + diag_add I
 __device__ __forceinline__ void gemm_set(int M, int N, int K, const Op &a, const Op &b,
                                          const MatView &c, int cr0, int cc0, bool lower,
                                          double diag_add, double *smem, GemmSync *gs) {
-  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, diag_add};
+  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, false, diag_add};
+  gemm_rt(ga, gemm_smem_align(smem), gs);
+}
+// C^T = A.B: element (i, j) of the product goes to the submatrix of `c` at (r0 + j, c0 + i).
+// Used to apply a 64 x 64 triangular inverse to a wide block (X = T X computed as X^T = X^T T^T,
+// so the long dimension runs over the 128-row tile side).
+__device__ __forceinline__ void gemm_set_t(int M, int N, int K, const Op &a, const Op &b,
+                                           const MatView &c, int cr0, int cc0, double *smem,
+                                           GemmSync *gs) {
+  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, false, false, true, 0.0};
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 
@@ -543,6 +557,130 @@ __device__ __forceinline__ int chol_diag(double *S, int64_t ld, int p0, int bw, 
   }
   __syncthreads();
   return bad;
+}
+
+
+// Inverse of the W x W (W <= 64) diagonal block of `src` at (p0, p0) written to Tg [64][64]
+// (global, zero outside W x W): two 32 x 32 diagonal inverses by substitution (warps 0 and 1,
+// lane = column), then the off-diagonal block from the 2 x 2 block formula
+//   lower:  [[A, 0], [C, B]]^-1 = [[A^-1, 0], [-B^-1 C A^-1, B^-1]]
+//   upper:  [[A, C], [0, B]]^-1 = [[A^-1, -A^-1 C B^-1], [0, B^-1]]
+__device__ __forceinline__ void tri_inv64(const double *src, int64_t ld, int p0, int W, int kind,
+                                          double *sm, double *Tg) {
+  double *Lb = sm, *Tb = sm + TB * TB_LD;
+  __syncthreads();
+  for (int q = threadIdx.x; q < TB * TB; q += NT) {
+    const int r = q / TB, c = q % TB;
+    double v = 0.0;
+    if (r < W && c < W) {
+      const bool keep = kind == TRI_UPPER ? (c >= r) : (kind == TRI_LOWER ? (c <= r) : (c < r));
+      if (keep) v = src[static_cast<int64_t>(p0 + r) * ld + p0 + c];
+      if (kind == TRI_UNIT_LOWER && r == c) v = 1.0;
+    } else if (r == c) {
+      v = 1.0;  // identity padding keeps the fixed-size substitution finite
+    }
+    Lb[r * TB_LD + c] = v;
+    Tb[r * TB_LD + c] = 0.0;
+  }
+  __syncthreads();
+  if (warp_id() < 2) {
+    const int o = 32 * warp_id(), c = lane_id();
+    double x[32];
+    if (kind != TRI_UPPER) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        double s = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < r; ++q) s = fma(-Lb[(o + r) * TB_LD + o + q], x[q], s);
+        x[r] = (kind == TRI_LOWER) ? s / Lb[(o + r) * TB_LD + o + r] : s;
+      }
+    } else {
+#pragma unroll
+      for (int r = 31; r >= 0; --r) {
+        double s = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = r + 1; q < 32; ++q) s = fma(-Lb[(o + r) * TB_LD + o + q], x[q], s);
+        x[r] = s / Lb[(o + r) * TB_LD + o + r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) Tb[(o + r) * TB_LD + o + c] = x[r];
+  }
+  __syncthreads();
+  // off-diagonal 32 x 32 block; P is staged in the block's unused (zero) quadrant of Tb
+  const bool upper = kind == TRI_UPPER;
+  for (int q = threadIdx.x; q < 32 * 32; q += NT) {
+    const int i = q / 32, j = q % 32;
+    double s = 0.0;
+    if (!upper) {  // P = C A^-1, C = Lb[32+i][k], A^-1 = Tb[k][j] (lower: k >= j)
+      for (int k = j; k < 32; ++k) s = fma(Lb[(32 + i) * TB_LD + k], Tb[k * TB_LD + j], s);
+      Tb[i * TB_LD + 32 + j] = s;
+    } else {       // P = C B^-1, C = Lb[i][32+k], B^-1 = Tb[32+k][32+j] (upper: k <= j)
+      for (int k = 0; k <= j; ++k) s = fma(Lb[i * TB_LD + 32 + k], Tb[(32 + k) * TB_LD + 32 + j], s);
+      Tb[(32 + i) * TB_LD + j] = s;
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 32 * 32; q += NT) {
+    const int i = q / 32, j = q % 32;
+    double s = 0.0;
+    if (!upper) {  // -B^-1 P, B^-1 = Tb[32+i][32+k] (k <= i), P[k][j] = Tb[k][32+j]
+      for (int k = 0; k <= i; ++k) s = fma(Tb[(32 + i) * TB_LD + 32 + k], Tb[k * TB_LD + 32 + j], s);
+      Lb[(32 + i) * TB_LD + j] = -s;  // result staged in Lb (its lower-left block is consumed)
+    } else {       // -A^-1 P, A^-1 = Tb[i][k] (k >= i), P[k][j] = Tb[32+k][j]
+      for (int k = i; k < 32; ++k) s = fma(Tb[i * TB_LD + k], Tb[(32 + k) * TB_LD + j], s);
+      Lb[i * TB_LD + 32 + j] = -s;
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < TB * TB; q += NT) {
+    const int r = q / TB, c = q % TB;
+    double v = 0.0;
+    if (r < W && c < W) {
+      const bool off = upper ? (r < 32 && c >= 32) : (r >= 32 && c < 32);
+      const bool zero = upper ? (r >= 32 && c < 32) : (r < 32 && c >= 32);
+      v = off ? Lb[r * TB_LD + c] : (zero ? 0.0 : Tb[r * TB_LD + c]);
+    }
+    Tg[q] = v;
+  }
+  __syncthreads();
+}
+
+// Unblocked Cholesky of the W x W (W <= 64) diagonal block S[p0.., p0..] (lower) in shared
+// memory, written back to S. Returns 1 if a non-positive pivot appears (S = I + K K^T is SPD).
+__device__ __forceinline__ int chol_diag64(double *S, int64_t ld, int p0, int W, double *sm) {
+  double *Lb = sm;
+  __shared__ int bad64;
+  __syncthreads();
+  if (threadIdx.x == 0) bad64 = 0;
+  for (int q = threadIdx.x; q < W * W; q += NT) {
+    const int r = q / W, c = q % W;
+    Lb[r * TB_LD + c] = c <= r ? S[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < W; ++c) {
+    const double d2 = Lb[c * TB_LD + c];
+    const double d = sqrt(d2);
+    __syncthreads();  // everyone has read the pivot before it is overwritten
+    if (threadIdx.x == 0) {
+      if (!(d2 > 0.0)) bad64 = 1;
+      Lb[c * TB_LD + c] = d;
+    }
+    for (int r = c + 1 + threadIdx.x; r < W; r += NT) Lb[r * TB_LD + c] /= d;
+    __syncthreads();
+    const int m = W - c - 1;  // trailing block rows/cols c+1..W-1, lower part
+    for (int q = threadIdx.x; q < m * m; q += NT) {
+      const int r = c + 1 + q / m, k = c + 1 + q % m;
+      if (k <= r) Lb[r * TB_LD + k] = fma(-Lb[r * TB_LD + c], Lb[k * TB_LD + c], Lb[r * TB_LD + k]);
+    }
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < W * W; q += NT) {
+    const int r = q / W, c = q % W;
+    if (c <= r) S[static_cast<int64_t>(p0 + r) * ld + p0 + c] = Lb[r * TB_LD + c];
+  }
+  __syncthreads();
+  return bad64;
 }
 
 }  // namespace la

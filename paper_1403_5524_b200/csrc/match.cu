@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int ldm = static_cast<int>(L.ldm), npad = static_cast<int>(L.npad);
   double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
   const MatView Mv{views + (blockIdx.x * 2 + 0) * NVIEW, slot + L.m_off, ldm};
-  const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, PB};
+  const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, TB};
   double *Mw = Mv.base;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
@@ -54,11 +54,11 @@ __global__ void __launch_bounds__(NT, 1)
     const double *Re = R + e * static_cast<int64_t>(n) * ldr;
     const double *Fe = F + e * n, *Ge = G + e * n, *Fpe = Fp + e * n, *Gpe = Gp + e * n;
 
-    // ---- S3: A_ij = G_i d_ij - a R_ij G'_j ; B_ij = F_i d_ij - a R_ij F'_j (4 loads in flight) ----
+    // ---- S3: A_ij = G_i d_ij - a R_ij G'_j ; B_ij = F_i d_ij - a R_ij F'_j (16 loads in flight) ----
     for (int i = warp_id(); i < n; i += NW) {
       const double *Ri = Re + static_cast<int64_t>(i) * ldr;
       double *Mi = Mw + static_cast<int64_t>(i) * ldm;
-      constexpr int U = 4;
+      constexpr int U = 8;
       for (int j0 = lane_id(); j0 < ncols; j0 += 32 * U) {
         double rv[U], sv[U];
 #pragma unroll
@@ -89,13 +89,17 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
 
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
+    // Outer blocks of W = 64 columns: two 32-wide panels (the second after a K = 32 update), then
+    // U12 = L11^{-1} A12 as ONE DMMA GEMM with the explicit 64 x 64 inverse (computed transposed,
+    // U12^T = A12^T L11^{-T}, so the long trailing dimension runs along the 128-row tiles), then the
+    // K = 64 trailing update. Every operand stays in the slot workspace (aligned, even pitch).
     int singular = 0;
     for (int P0 = 0; P0 < n; P0 += NB) {
       const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
       singular |= panel_lu(Mw, ldm, n, P0, w1, P0, ncols, sm.ipiv, sm.redv, sm.redi);
-      tri_inv(Mw, ldm, P0, w1, TRI_UNIT_LOWER, sm.tri, Tv.base);  // L_aa^{-1}
       if (w2 > 0) {
-        // right half of the outer block: U_ab = L_aa^{-1} A_ab ; A_.b -= L_.a U_ab ; factor it
+        // right half of the outer block: U_ab = L_aa^{-1} A_ab (32 x 32); A_.b -= L_.a U_ab
+        tri_inv64(Mw, ldm, P0, w1, TRI_UNIT_LOWER, sm.tri, Tv.base);
         gemm_set(w1, w2, w1, opk(Tv, 0, 0), opn(Mv, P0, P0 + w1), Mv, P0, P0 + w1, false, 0.0, smg, gs);
         gemm_sub(n - P0 - w1, w2, w1, opk(Mv, P0 + w1, P0), opn(Mv, P0, P0 + w1), Mv, P0 + w1,
                  P0 + w1, false, smg, gs);
@@ -106,13 +110,9 @@ __global__ void __launch_bounds__(NT, 1)
       const int ct = min((P0 + W + 1) & ~1, ncols);
       const int nt = ncols - ct;
       if (nt > 0) {
-        // U12 = L11^{-1} A12, L11 = [[L_aa, 0], [L_ba, L_bb]]
-        gemm_set(w1, nt, w1, opk(Tv, 0, 0), opn(Mv, P0, ct), Mv, P0, ct, false, 0.0, smg, gs);
-        if (w2 > 0) {
-          gemm_sub(w2, nt, w1, opk(Mv, P0 + w1, P0), opn(Mv, P0, ct), Mv, P0 + w1, ct, false, smg, gs);
-          tri_inv(Mw, ldm, P0 + w1, w2, TRI_UNIT_LOWER, sm.tri, Tv.base);  // L_bb^{-1}
-          gemm_set(w2, nt, w2, opk(Tv, 0, 0), opn(Mv, P0 + w1, ct), Mv, P0 + w1, ct, false, 0.0, smg, gs);
-        }
+        tri_inv64(Mw, ldm, P0, W, TRI_UNIT_LOWER, sm.tri, Tv.base);  // L11^{-1}
+        // U12^T = A12^T L11^{-T}: A'(j, k) = M[P0+k][ct+j], B'(i, k) = Tg[i][k]; stored transposed
+        gemm_set_t(nt, W, W, opn(Mv, P0, ct), opk(Tv, 0, 0), Mv, P0, ct, smg, gs);
         // trailing update with K = W
         if (P0 + W < n)
           gemm_sub(n - P0 - W, nt, W, opk(Mv, P0 + W, P0), opn(Mv, P0, ct), Mv, P0 + W, ct, false,
@@ -123,15 +123,9 @@ __global__ void __launch_bounds__(NT, 1)
     // ---- S4b: blocked back substitution U Y = L^{-1} P B_open (Y = columns [npad, npad+o)) ----
     if (o > 0) {
       for (int P0 = ((n - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
-        const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
-        if (w2 > 0) {
-          tri_inv(Mw, ldm, P0 + w1, w2, TRI_UPPER, sm.tri, Tv.base);  // U_bb^{-1}
-          gemm_set(w2, o, w2, opk(Tv, 0, 0), opn(Mv, P0 + w1, npad), Mv, P0 + w1, npad, false, 0.0,
-                   smg, gs);
-          gemm_sub(w1, o, w2, opk(Mv, P0, P0 + w1), opn(Mv, P0 + w1, npad), Mv, P0, npad, false, smg, gs);
-        }
-        tri_inv(Mw, ldm, P0, w1, TRI_UPPER, sm.tri, Tv.base);  // U_aa^{-1}
-        gemm_set(w1, o, w1, opk(Tv, 0, 0), opn(Mv, P0, npad), Mv, P0, npad, false, 0.0, smg, gs);
+        const int W = min(NB, n - P0);
+        tri_inv64(Mw, ldm, P0, W, TRI_UPPER, sm.tri, Tv.base);  // U_pp^{-1}
+        gemm_set_t(o, W, W, opn(Mv, P0, npad), opk(Tv, 0, 0), Mv, P0, npad, smg, gs);
         if (P0 > 0)
           gemm_sub(P0, o, W, opk(Mv, 0, P0), opn(Mv, P0, npad), Mv, 0, npad, false, smg, gs);
       }
@@ -169,7 +163,7 @@ int64_t match_ws_doubles_per_slot(int64_t nch) { return match_layout(nch).slot; 
 // Matrices of one slot whose TMA descriptors the kernel uses: (M, Tg), NVIEW box shapes each.
 void match_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
   const MatchLayout L = match_layout(nch);
-  specs = {MatSpec{L.m_off, nch, L.ldm, L.ldm}, MatSpec{L.tg_off, 32, 32, 32}};
+  specs = {MatSpec{L.m_off, nch, L.ldm, L.ldm}, MatSpec{L.tg_off, TB, TB, TB}};
 }
 
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,

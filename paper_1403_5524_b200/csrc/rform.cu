@@ -154,12 +154,12 @@ __global__ void __launch_bounds__(C::NT, 1)
         for (int ni = 0; ni < C::NI; ++ni)
           lds128(b[ni][0], b[ni][1], bbase + kb * C::BOX_BYTES + brow[ni] + chunk);
 #pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int ni = 0; ni < C::NI; ++ni) {
-            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][0], b[ni][0]);
-            dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][1], b[ni][1]);
-          }
+          for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < C::NI; ++ni)
+              dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][h], b[ni][h]);
       }
     }
     __syncwarp();

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NT, 1)
   const MatView Sv{vw + 0 * NVIEW, slot + L.s_off, ldo};
   const MatView Xv{vw + 1 * NVIEW, slot + L.x_off, ldo};
   const MatView Kv{vw + 2 * NVIEW, slot + L.k_off, ldo};
-  const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, PB};
+  const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, TB};
   double *S = Sv.base, *Tg = Tv.base;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
@@ -57,64 +57,52 @@ __global__ void __launch_bounds__(NT, 1)
     int bad = 0;
     if (o > 0) {
       // Kc = X = K_oo (aligned, even pitch: operands of the TMA GEMM pipeline)
-      for (int i = warp_id(); i < o; i += NW)
-        for (int j = lane_id(); j < o; j += 32) {
-          const double v = Ke[static_cast<int64_t>(i) * ldk + j];
-          *Kv.at(i, j) = v;
-          *Xv.at(i, j) = v;
+      for (int i = warp_id(); i < o; i += NW) {
+        const double *src = Ke + static_cast<int64_t>(i) * ldk;
+        double *dk = Kv.at(i, 0), *dx = Xv.at(i, 0);
+        constexpr int U = 8;  // 8 independent loads in flight per lane
+        for (int j0 = lane_id(); j0 < o; j0 += 32 * U) {
+          double v[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) v[q] = (j0 + 32 * q < o) ? src[j0 + 32 * q] : 0.0;
+#pragma unroll
+          for (int q = 0; q < U; ++q)
+            if (j0 + 32 * q < o) {
+              dk[j0 + 32 * q] = v[q];
+              dx[j0 + 32 * q] = v[q];
+            }
         }
+      }
       __syncthreads();
       // S = I + K_oo K_oo^T (lower tiles)
       gemm_set(o, o, o, opk(Kv, 0, 0), opk(Kv, 0, 0), Sv, 0, 0, true, 1.0, smg, gs);
-      // blocked Cholesky S = L L^T (lower); panel solves L21 = S21 L11^{-T} as in-place GEMMs
+      // blocked Cholesky S = L L^T (lower), 64-wide blocks: diagonal block in smem, then
+      // L21 = S21 L11^{-T} as one in-place GEMM with the explicit inverse, then the K = 64 update
       for (int P0 = 0; P0 < o; P0 += NB) {
-        const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
-        bad |= chol_diag(S, ldo, P0, w1, sm.tri);
-        tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
-        if (P0 + w1 < o)
-          gemm_set(o - P0 - w1, w1, w1, opk(Sv, P0 + w1, P0), opk(Tv, 0, 0), Sv, P0 + w1, P0, false,
-                   0.0, smg, gs);
-        if (w2 > 0) {
-          gemm_sub(o - P0 - w1, w2, w1, opk(Sv, P0 + w1, P0), opk(Sv, P0 + w1, P0), Sv, P0 + w1,
-                   P0 + w1, false, smg, gs);
-          bad |= chol_diag(S, ldo, P0 + w1, w2, sm.tri);
-          if (P0 + W < o) {
-            tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
-            gemm_set(o - P0 - W, w2, w2, opk(Sv, P0 + W, P0 + w1), opk(Tv, 0, 0), Sv, P0 + W, P0 + w1,
-                     false, 0.0, smg, gs);
-          }
-        }
+        const int W = min(NB, o - P0);
+        bad |= chol_diag64(S, ldo, P0, W, sm.tri);
         if (P0 + W < o) {
+          tri_inv64(S, ldo, P0, W, TRI_LOWER, sm.tri, Tg);
+          gemm_set(o - P0 - W, W, W, opk(Sv, P0 + W, P0), opk(Tv, 0, 0), Sv, P0 + W, P0, false, 0.0,
+                   smg, gs);
           const int m2 = o - P0 - W;
           gemm_sub(m2, m2, W, opk(Sv, P0 + W, P0), opk(Sv, P0 + W, P0), Sv, P0 + W, P0 + W, true,
                    smg, gs);
         }
       }
-      // forward: L Z = K  (X holds K_oo)
+      // forward: L Z = K  (X holds K_oo); X_p = L_pp^{-1} X_p as X_p^T = X_p^T L_pp^{-T}
       for (int P0 = 0; P0 < o; P0 += NB) {
-        const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
-        tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
-        gemm_set(w1, o, w1, opk(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
-        if (w2 > 0) {
-          gemm_sub(w2, o, w1, opk(Sv, P0 + w1, P0), opn(Xv, P0, 0), Xv, P0 + w1, 0, false, smg, gs);
-          tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
-          gemm_set(w2, o, w2, opk(Tv, 0, 0), opn(Xv, P0 + w1, 0), Xv, P0 + w1, 0, false, 0.0, smg, gs);
-        }
+        const int W = min(NB, o - P0);
+        tri_inv64(S, ldo, P0, W, TRI_LOWER, sm.tri, Tg);
+        gemm_set_t(o, W, W, opn(Xv, P0, 0), opk(Tv, 0, 0), Xv, P0, 0, smg, gs);
         if (P0 + W < o)
           gemm_sub(o - P0 - W, o, W, opk(Sv, P0 + W, P0), opn(Xv, P0, 0), Xv, P0 + W, 0, false, smg, gs);
       }
-      // backward: L^T X = Z
+      // backward: L^T X = Z; X_p = L_pp^{-T} X_p as X_p^T = X_p^T L_pp^{-1}: B'(i, k) = Tg[k][i]
       for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
-        const int W = min(NB, o - P0), w1 = min(PB, W), w2 = W - w1;
-        if (w2 > 0) {
-          tri_inv(S, ldo, P0 + w1, w2, TRI_LOWER, sm.tri, Tg);
-          // X_b = L_bb^{-T} X_b : A(m,k) = Tg[k][m]
-          gemm_set(w2, o, w2, opn(Tv, 0, 0), opn(Xv, P0 + w1, 0), Xv, P0 + w1, 0, false, 0.0, smg, gs);
-          // X_a -= (L[P0+w1:P0+W, P0:P0+w1])^T X_b
-          gemm_sub(w1, o, w2, opn(Sv, P0 + w1, P0), opn(Xv, P0 + w1, 0), Xv, P0, 0, false, smg, gs);
-        }
-        tri_inv(S, ldo, P0, w1, TRI_LOWER, sm.tri, Tg);
-        gemm_set(w1, o, w1, opn(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
+        const int W = min(NB, o - P0);
+        tri_inv64(S, ldo, P0, W, TRI_LOWER, sm.tri, Tg);
+        gemm_set_t(o, W, W, opn(Xv, P0, 0), opn(Tv, 0, 0), Xv, P0, 0, smg, gs);
         if (P0 > 0)
           // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]
           gemm_sub(P0, o, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
@@ -125,16 +113,27 @@ __global__ void __launch_bounds__(NT, 1)
     // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
       double s = 0.0;
-      for (int j = lane_id(); j < n; j += 32) {
-        double v = 0.0;
-        if (i < o && j < o) {
-          const double x = *Xv.at(i, j);
-          const double p = *Sv.at(i, j);
-          v = 4.0 * fma(x, x, p * p);
-          if (!isfinite(v)) bad = 1;
+      const double *xr = Xv.at(i, 0), *pr = Sv.at(i, 0);
+      constexpr int U = 4;  // 2U independent loads in flight per lane
+      for (int j0 = lane_id(); j0 < n; j0 += 32 * U) {
+        double xv[U], pv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int j = j0 + 32 * q;
+          const bool in = i < o && j < o;
+          xv[q] = in ? xr[j] : 0.0;
+          pv[q] = in ? pr[j] : 0.0;
         }
-        if (T2e) T2e[static_cast<int64_t>(i) * n + j] = v;
-        s += v;
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int j = j0 + 32 * q;
+          if (j < n) {
+            const double v = 4.0 * fma(xv[q], xv[q], pv[q] * pv[q]);
+            if (!isfinite(v)) bad = 1;
+            if (T2e) T2e[static_cast<int64_t>(i) * n + j] = v;
+            s += v;
+          }
+        }
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -151,7 +150,7 @@ int64_t tepi_ws_doubles_per_slot(int64_t nch) { return tepi_layout(nch).slot; }
 void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
   const TepiLayout L = tepi_layout(nch);
   specs = {MatSpec{L.s_off, nch, L.ldo, L.ldo}, MatSpec{L.x_off, nch, L.ldo, L.ldo},
-           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, 32, 32, 32}};
+           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, TB, TB, TB}};
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
