@@ -62,4 +62,4 @@ def test_sass_is_sm100a_with_dmma_and_tma(lib):
     assert "sm_100a" in sass
     assert "DMMA.8x8x4" in sass          # FP64 tensor-core MMA in R formation / LU / Cholesky
     assert "UTMALDG" in sass             # TMA tile loads (cp.async.bulk.tensor) in R formation
-    assert "LDGSTS" in sass              # cp.async staging in the per-energy dense LA
+    assert "UBLKCP" in sass              # cp.async.bulk C-tile copies in the per-energy dense LA
