@@ -22,6 +22,35 @@ struct TepiSmem {
 };
 
 
+// P[j][i] = P[i][j] for j > i (upper triangle from the lower one), 32x32 blocks staged through
+// shared memory so that both the reads and the writes are coalesced row segments.
+__device__ __forceinline__ void mirror_lower(double *P, int64_t ld, int o, double *smem) {
+  constexpr int TL = 33;
+  const int nb = (o + 31) / 32;
+  double *tile = smem + warp_id() * 32 * TL;  // one 32x33 tile per warp
+  const int lane = lane_id();
+  __syncthreads();
+  for (int b = warp_id(); b < nb * (nb + 1) / 2; b += NW) {
+    int bi = 0, rem = b;
+    while (rem > bi) {
+      rem -= bi + 1;
+      ++bi;
+    }
+    const int bj = rem;  // bj <= bi: lower block (bi, bj) -> upper block (bj, bi)
+    for (int r = 0; r < 32; ++r) {
+      const int gi = bi * 32 + r, gj = bj * 32 + lane;
+      tile[r * TL + lane] = (gi < o && gj < o) ? P[static_cast<int64_t>(gi) * ld + gj] : 0.0;
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; ++r) {  // row r of the upper block = column r of the lower block
+      const int gi = bj * 32 + r, gj = bi * 32 + lane;
+      if (gi < o && gj < o && gj > gi) P[static_cast<int64_t>(gi) * ld + gj] = tile[lane * TL + r];
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // Workspace slot: S (then P) [o][ldo], X [o][ldo], Kc [o][ldo] (aligned copy of K_oo),
 // Tg [32][32] (inverse of a 32x32 diagonal block of L: triangular solves run as DMMA GEMMs).
 // Factorisation / solves use outer blocks of NB = 64 (two inner 32-wide triangles) so that the
@@ -107,8 +136,9 @@ __global__ void __launch_bounds__(NT, 1)
           // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]
           gemm_sub(P0, o, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
       }
-      // P = K_oo X  (into S's storage)
-      gemm_set(o, o, o, opk(Kv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, false, 0.0, smg, gs);
+      // P = K_oo X = K S^{-1} K is symmetric: lower tiles only (half the flops), then mirrored
+      gemm_set(o, o, o, opk(Kv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, true, 0.0, smg, gs);
+      mirror_lower(S, ldo, o, sm.gemm);
     }
     // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
