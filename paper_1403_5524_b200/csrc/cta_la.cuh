@@ -33,7 +33,7 @@ constexpr int STAGES = 3;                     // A/B ring depth
 constexpr int NVIEW = 3;
 constexpr int A_STAGE_BYTES = BM * BK * 8, B_STAGE_BYTES = BN * BK * 8;
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int CS_LD = BN + 8;  // C tile pitch in smem (bulk row copies)
+constexpr int CS_LD = BN + 2;  // C tile pitch (bulk row copies): 4 rows = 64 mod 128 bytes apart
 constexpr int C_ELEMS = BM * CS_LD;
 constexpr int GEMM_SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_ELEMS * 8;  // + 1024 alignment slack
 constexpr int GEMM_SMEM_DOUBLES = GEMM_SMEM_BYTES / 8;
@@ -106,11 +106,12 @@ struct GemmArgs {
 // k-contiguous fragments are read as 16-byte (k, k+1) pairs; within each 8-row group fragment row
 // g maps to smem row (g>>1) + 4(g&1) so those reads are bank-conflict free under the swizzle.
 // Partial k-slices are masked (both operands zeroed beyond K).
-static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al, GemmSync *gs) {
+template <bool A_KC, bool B_KC>
+static __device__ __noinline__ void gemm_impl(const GemmArgs &ga, uint8_t *smem_al, GemmSync *gs) {
   const int M = ga.M, N = ga.N, K = ga.K;
-  const bool A_KC = ga.a.kc, B_KC = ga.b.kc, lower = ga.lower, readC = ga.read_c;
+  const bool lower = ga.lower, readC = ga.read_c;
   __syncthreads();
-  if (M <= 0 || N <= 0 || K <= 0) return;  // K == 0 only comes with C = 0 * ... never used
+  if (M <= 0 || N <= 0 || K <= 0) return;
   if (threadIdx.x == 0) {
     for (int st = 0; st < STAGES; ++st) {
       mbar_init(&gs->full[st], 1);
@@ -125,17 +126,7 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al
   const int nkc = cdiv(K, BK);
   int ntiles = 0;
   for (int tm = 0; tm < tiles_m; ++tm) ntiles += tiles_in_row(tm, tiles_n, lower);
-  const int total = ntiles * nkc;
   double *Cs = reinterpret_cast<double *>(smem_al + STAGES * STAGE_BYTES);
-  auto decode_tile = [&](int tile, int &tm, int &tn) {
-    tm = 0;
-    int cnt;
-    while (tile >= (cnt = tiles_in_row(tm, tiles_n, lower))) {
-      tile -= cnt;
-      ++tm;
-    }
-    tn = tile;
-  };
   const int warp = warp_id(), lane = lane_id();
 
   if (warp == NCW) {
@@ -149,12 +140,13 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al
       tma_prefetch_desc(tmA);
       tma_prefetch_desc(tmB);
     }
-    for (int it = 0; it < total; ++it) {
-      const int st = it % STAGES, use = it / STAGES;
-      const int tile = it / nkc, kc = it % nkc;
-      int tm, tn;
-      decode_tile(tile, tm, tn);
-      if (kc == 0 && readC) {
+    int it = 0, tm = 0, tn = 0, rowcnt = tiles_in_row(0, tiles_n, lower);
+    for (int tile = 0; tile < ntiles; ++tile) {
+      if (tn == rowcnt) {
+        tn = 0;
+        rowcnt = tiles_in_row(++tm, tiles_n, lower);
+      }
+      if (readC) {
         if (tile > 0) mbar_wait(&gs->cempty, (tile - 1) & 1);
         const int rows = min(BM, M - tm * BM), cols = min(BN, N - tn * BN);
         const uint32_t rb = round16(cols * 8);
@@ -163,151 +155,202 @@ static __device__ __noinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al
         bulk_rows(Cs, CS_LD, ga.C + static_cast<int64_t>(tm * BM) * ga.ldc + tn * BN, ga.ldc, rows,
                   rb, &gs->cfull);
       }
-      if (it >= STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
-      if (lane == 0) {
-        const int k0 = kc * BK;
-        uint64_t *bar = &gs->full[st];
-        mbar_arrive_expect_tx(bar, STAGE_BYTES);
-        const uint32_t sa = smem_u32(smem_al + st * STAGE_BYTES), sb = sa + A_STAGE_BYTES;
-        if (A_KC) {
+      for (int kc = 0; kc < nkc; ++kc, ++it) {
+        const int st = it % STAGES, use = it / STAGES;
+        if (it >= STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
+        if (lane == 0) {
+          const int k0 = kc * BK;
+          uint64_t *bar = &gs->full[st];
+          mbar_arrive_expect_tx(bar, STAGE_BYTES);
+          const uint32_t sa = smem_u32(smem_al + st * STAGE_BYTES), sb = sa + A_STAGE_BYTES;
+          if (A_KC) {
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
-            tma_load_2d(sa + q * (BM * 128), tmA, bar, ga.a.c0 + k0 + 16 * q, ga.a.r0 + tm * BM);
-        } else {
+            for (int q = 0; q < 2; ++q)
+              tma_load_2d(sa + q * (BM * 128), tmA, bar, ga.a.c0 + k0 + 16 * q, ga.a.r0 + tm * BM);
+          } else {
 #pragma unroll
-          for (int q = 0; q < BM / 16; ++q)
-            tma_load_2d(sa + q * (BK * 128), tmA, bar, ga.a.c0 + tm * BM + 16 * q, ga.a.r0 + k0);
+            for (int q = 0; q < BM / 16; ++q)
+              tma_load_2d(sa + q * (BK * 128), tmA, bar, ga.a.c0 + tm * BM + 16 * q, ga.a.r0 + k0);
+          }
+          if (B_KC) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              tma_load_2d(sb + q * (BN * 128), tmB, bar, ga.b.c0 + k0 + 16 * q, ga.b.r0 + tn * BN);
+          } else {
+#pragma unroll
+            for (int q = 0; q < BN / 16; ++q)
+              tma_load_2d(sb + q * (BK * 128), tmB, bar, ga.b.c0 + tn * BN + 16 * q, ga.b.r0 + k0);
+          }
         }
-        if (B_KC) {
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            tma_load_2d(sb + q * (BN * 128), tmB, bar, ga.b.c0 + k0 + 16 * q, ga.b.r0 + tn * BN);
-        } else {
-#pragma unroll
-          for (int q = 0; q < BN / 16; ++q)
-            tma_load_2d(sb + q * (BK * 128), tmB, bar, ga.b.c0 + tn * BN + 16 * q, ga.b.r0 + k0);
-        }
+        __syncwarp();
       }
-      __syncwarp();
+      ++tn;
     }
   } else {
     // ============================ consumer warps ============================
     const int wm = warp % WM, wn = warp / WM;
     const int g = lane >> 2, t = lane & 3;
     const int pg = frag_perm(g);
-    const int arow = A_KC ? pg : g;  // smem row / m offset of this lane's A fragment rows
-    // local (row, col) of acc[mi][ni][h] inside the tile
-    auto acc_row = [&](int mi) { return wm * WTM + mi * 8 + arow; };
-    auto acc_col = [&](int ni, int h) { return wn * WTN + ni * 8 + (B_KC ? t + 4 * h : 2 * t + h); };
-    double acc[MI][NI][2];
-    for (int it = 0; it < total; ++it) {
-      const int st = it % STAGES, use = it / STAGES;
-      const int tile = it / nkc, kc = it % nkc;
-      int tm, tn;
-      decode_tile(tile, tm, tn);
-      if (kc == 0) {
-        if (readC) {
-          mbar_wait(&gs->cfull, tile & 1);
+    // per-lane byte offsets of the fragment loads inside a stage (k8 = 0; add k8 terms below)
+    //   KC  : box (k8>>1) at +k8h*box, row r (r & 7 = pg), 16-byte chunk ((k8&1)*4 + t) ^ pg
+    //   !KC : box m>>4, row k = 8 k8 + 2t (+1) -> (k & 7) = 2t (+1) is k8-independent
+    uint32_t aoff[MI][2], boff[NI][2];
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) {
-              const double *cr = Cs + acc_row(mi) * CS_LD;
-              acc[mi][ni][0] = -cr[acc_col(ni, 0)];  // C -= A.B as acc = -C; acc += A.B; C = -acc
-              acc[mi][ni][1] = -cr[acc_col(ni, 1)];
-            }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&gs->cempty);
-        } else {
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-        }
+    for (int mi = 0; mi < MI; ++mi) {
+      if (A_KC) {
+        const int r = wm * WTM + mi * 8 + pg;
+        aoff[mi][0] = r * 128 + ((t ^ pg) << 4);
+        aoff[mi][1] = r * 128 + (((4 + t) ^ pg) << 4);
+      } else {
+        const int m = wm * WTM + mi * 8 + g, j2 = (m & 15) >> 1;
+        const uint32_t base = (m >> 4) * (BK * 128) + ((m & 1) << 3);
+        aoff[mi][0] = base + (2 * t) * 128 + ((j2 ^ (2 * t)) << 4);
+        aoff[mi][1] = base + (2 * t + 1) * 128 + ((j2 ^ (2 * t + 1)) << 4);
       }
-      mbar_wait(&gs->full[st], use & 1);
-      const int krem = min(BK, K - kc * BK);
-      const uint32_t sa = smem_u32(smem_al + st * STAGE_BYTES), sb = sa + A_STAGE_BYTES;
-#pragma unroll 1
-      for (int k8 = 0; k8 < BK / 8; ++k8) {
-        if (k8 * 8 >= krem) break;
-        const int k = k8 * 8 + 2 * t;  // this lane's k pair (k, k+1) for the two DMMAs
-        double a[MI][2], b[NI][2];
+    }
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      if (B_KC) {
+        const int r = wn * WTN + ni * 8 + pg;
+        boff[ni][0] = r * 128 + ((t ^ pg) << 4);
+        boff[ni][1] = r * 128 + (((4 + t) ^ pg) << 4);
+      } else {
+        const int n = wn * WTN + ni * 8 + g, j2 = (n & 15) >> 1;
+        const uint32_t base = (n >> 4) * (BK * 128) + ((n & 1) << 3);
+        boff[ni][0] = base + (2 * t) * 128 + ((j2 ^ (2 * t)) << 4);
+        boff[ni][1] = base + (2 * t + 1) * 128 + ((j2 ^ (2 * t + 1)) << 4);
+      }
+    }
+    const int arow = A_KC ? pg : g;  // tile-local row offset of this lane's accumulator rows
+    const uint32_t smem0 = smem_u32(smem_al);
+    double acc[MI][NI][2];
+    int it = 0, tm = 0, tn = 0, rowcnt = tiles_in_row(0, tiles_n, lower);
+    for (int tile = 0; tile < ntiles; ++tile) {
+      if (tn == rowcnt) {
+        tn = 0;
+        rowcnt = tiles_in_row(++tm, tiles_n, lower);
+      }
+      if (readC) {
+        mbar_wait(&gs->cfull, tile & 1);
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
-          if (A_KC) {
-            const int r = wm * WTM + mi * 8 + pg;  // r & 7 == pg
-            const uint32_t chunk = static_cast<uint32_t>((((k8 & 1) * 4 + t) ^ pg) << 4);
-            lds128(a[mi][0], a[mi][1], sa + (k8 >> 1) * (BM * 128) + r * 128 + chunk);
-          } else {
-            const int m = wm * WTM + mi * 8 + g;
-            const uint32_t base = sa + (m >> 4) * (BK * 128) + ((m & 1) << 3);
-            const int j2 = (m & 15) >> 1;
-            a[mi][0] = lds64(base + k * 128 + ((j2 ^ (k & 7)) << 4));
-            a[mi][1] = lds64(base + (k + 1) * 128 + ((j2 ^ ((k + 1) & 7)) << 4));
-          }
-        }
+          const double *cr = Cs + (wm * WTM + mi * 8 + arow) * CS_LD + wn * WTN;
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          if (B_KC) {
-            const int r = wn * WTN + ni * 8 + pg;
-            const uint32_t chunk = static_cast<uint32_t>((((k8 & 1) * 4 + t) ^ pg) << 4);
-            lds128(b[ni][0], b[ni][1], sb + (k8 >> 1) * (BN * 128) + r * 128 + chunk);
-          } else {
-            const int n = wn * WTN + ni * 8 + g;
-            const uint32_t base = sb + (n >> 4) * (BK * 128) + ((n & 1) << 3);
-            const int j2 = (n & 15) >> 1;
-            b[ni][0] = lds64(base + k * 128 + ((j2 ^ (k & 7)) << 4));
-            b[ni][1] = lds64(base + (k + 1) * 128 + ((j2 ^ ((k + 1) & 7)) << 4));
+          for (int ni = 0; ni < NI; ++ni) {
+            double c0, c1;
+            if (B_KC) {
+              c0 = cr[ni * 8 + t];
+              c1 = cr[ni * 8 + t + 4];
+            } else {
+              lds128(c0, c1, smem_u32(cr + ni * 8 + 2 * t));
+            }
+            acc[mi][ni][0] = -c0;  // C -= A.B as acc = -C; acc += A.B; C = -acc (exact)
+            acc[mi][ni][1] = -c1;
           }
         }
-        if (k8 * 8 + 8 > krem) {  // partial slice: zero both operands beyond K
-          const bool v0 = k < krem, v1 = k + 1 < krem;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&gs->cempty);
+      } else {
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+      for (int kc = 0; kc < nkc; ++kc, ++it) {
+        const int st = it % STAGES, use = it / STAGES;
+        mbar_wait(&gs->full[st], use & 1);
+        const int krem = min(BK, K - kc * BK);
+        const uint32_t sa = smem0 + st * STAGE_BYTES, sb = sa + A_STAGE_BYTES;
+        auto step = [&](const int k8, const bool partial) {
+          double a[MI][2], b[NI][2];
 #pragma unroll
           for (int mi = 0; mi < MI; ++mi) {
-            a[mi][0] = v0 ? a[mi][0] : 0.0;
-            a[mi][1] = v1 ? a[mi][1] : 0.0;
+            if (A_KC) {
+              lds128(a[mi][0], a[mi][1], sa + (k8 >> 1) * (BM * 128) + aoff[mi][k8 & 1]);
+            } else {
+              a[mi][0] = lds64(sa + k8 * 1024 + aoff[mi][0]);
+              a[mi][1] = lds64(sa + k8 * 1024 + aoff[mi][1]);
+            }
           }
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) {
-            b[ni][0] = v0 ? b[ni][0] : 0.0;
-            b[ni][1] = v1 ? b[ni][1] : 0.0;
-          }
-        }
-        // k-slot 0 for all 16 accumulators, then k-slot 1: dependent DMMAs are 16 issues apart
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][h], b[ni][h]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&gs->empty[st]);
-      if (kc == nkc - 1) {
-#pragma unroll
-        for (int mi = 0; mi < MI; ++mi) {
-          const int r = tm * BM + acc_row(mi);
-          if (r >= M) continue;
-          double *crow = ga.C + static_cast<int64_t>(r) * ga.ldc;
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = tn * BN + acc_col(ni, h);
-              if (c >= N) continue;
-              if (readC)
-                crow[c] = -acc[mi][ni][h];
-              else if (ga.trans_c)
-                ga.C[static_cast<int64_t>(c) * ga.ldc + r] = acc[mi][ni][h];
-              else
-                crow[c] = acc[mi][ni][h] + (r == c ? ga.diag_add : 0.0);
+            if (B_KC) {
+              lds128(b[ni][0], b[ni][1], sb + (k8 >> 1) * (BN * 128) + boff[ni][k8 & 1]);
+            } else {
+              b[ni][0] = lds64(sb + k8 * 1024 + boff[ni][0]);
+              b[ni][1] = lds64(sb + k8 * 1024 + boff[ni][1]);
             }
+          }
+          if (partial) {  // zero both operands beyond K (stale smem may hold anything)
+            const int k = k8 * 8 + 2 * t;
+            const bool v0 = k < krem, v1 = k + 1 < krem;
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+              a[mi][0] = v0 ? a[mi][0] : 0.0;
+              a[mi][1] = v1 ? a[mi][1] : 0.0;
+            }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+              b[ni][0] = v0 ? b[ni][0] : 0.0;
+              b[ni][1] = v1 ? b[ni][1] : 0.0;
+            }
+          }
+          // k-slot 0 for all 16 accumulators, then k-slot 1: dependent DMMAs are 16 issues apart
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][h], b[ni][h]);
+        };
+        if (krem == BK) {
+#pragma unroll
+          for (int k8 = 0; k8 < BK / 8; ++k8) step(k8, false);
+        } else {
+#pragma unroll 1
+          for (int k8 = 0; k8 * 8 < krem; ++k8) step(k8, true);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&gs->empty[st]);
       }
+      // epilogue: this warp's 32 x 32 part of the tile straight to global memory
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const int r = tm * BM + wm * WTM + mi * 8 + arow;
+        if (r >= M) continue;
+        double *crow = ga.C + static_cast<int64_t>(r) * ga.ldc;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = tn * BN + wn * WTN + ni * 8 + (B_KC ? t + 4 * h : 2 * t + h);
+            if (c >= N) continue;
+            if (readC)
+              crow[c] = -acc[mi][ni][h];
+            else if (ga.trans_c)
+              ga.C[static_cast<int64_t>(c) * ga.ldc + r] = acc[mi][ni][h];
+            else
+              crow[c] = acc[mi][ni][h] + (r == c ? ga.diag_add : 0.0);
+          }
+      }
+      ++tn;
     }
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void gemm_rt(const GemmArgs &ga, uint8_t *smem_al, GemmSync *gs) {
+  if (ga.a.kc) {
+    if (ga.b.kc)
+      gemm_impl<true, true>(ga, smem_al, gs);
+    else
+      gemm_impl<true, false>(ga, smem_al, gs);
+  } else {
+    if (ga.b.kc)
+      gemm_impl<false, true>(ga, smem_al, gs);
+    else
+      gemm_impl<false, false>(ga, smem_al, gs);
+  }
 }
 
 // Front ends (one compiled instance of the pipeline for every call site).
