@@ -413,95 +413,142 @@ __device__ __forceinline__ void block_argmax(double &v, int &idx, double *redv, 
 }
 
 // LU with partial pivoting of the panel M[p0:n, p0:p0+bw] (bw <= 32), in place: multipliers
-// below the diagonal, U on and above. Each interchange swaps the two rows over the columns
-// [sc0, sc1) (the whole augmented row right of the current outer block, so the trailing matrix,
-// the right-hand sides and the outer block's earlier multipliers stay consistent); the pivot rows
-// are also recorded in ipiv[0..bw). Returns 1 on an exact zero pivot. The rank-1 update of column
-// j is fused with the pivot search of column j+1 (one pass over the rows per column).
-// Pivot rule: max |a_ij|, ties -> lowest row (the oracle's rule).
+// below the diagonal, U on and above; pivot rows (absolute) in ipiv[0..bw). Returns 1 on an exact
+// zero pivot. Pivot rule: max |a_ij| over the remaining rows, ties -> lowest row (the oracle's rule).
+// The panel is processed in sub-panels of SPW = 8 columns held in shared memory (sp: >= (n-p0)*9
+// doubles): each sub-panel is factored entirely in smem (pivot search, row swap, rank-1 update per
+// column), written back, its interchanges are applied to the whole augmented rows [sc0, sc1) in
+// order, and the panel's remaining columns get one rank-8 update pass (U rows by a unit-lower 8x8
+// solve). Global memory is touched ~4 times per 32 columns instead of once per column.
+constexpr int SPW = 8, SP_LD = SPW + 1;
 __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, int bw, int sc0,
-                                            int sc1, int *ipiv, double *redv, int *redi) {
+                                        int sc1, int *ipiv, double *sp, double *ubuf, double *redv,
+                                        int *redi) {
   const int warp = warp_id(), lane = lane_id();
   int singular = 0;
-  double best = -1.0;
-  int besti = n;
-  for (int i = p0 + threadIdx.x; i < n; i += NT) {
-    const double v = fabs(M[static_cast<int64_t>(i) * ld + p0]);
-    if (v > best) {
-      best = v;
-      besti = i;
+  for (int s0 = 0; s0 < bw; s0 += SPW) {
+    const int c0 = p0 + s0, w = min(SPW, bw - s0), nr = n - c0;
+    // 1. stage the sub-panel rows c0..n-1, columns c0..c0+w
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * SPW; q += NT) {
+      const int r = q / SPW, c = q % SPW;
+      sp[r * SP_LD + c] = c < w ? M[static_cast<int64_t>(c0 + r) * ld + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    // 2. factor in shared memory
+    for (int jj = 0; jj < w; ++jj) {
+      double best = -1.0;
+      int besti = nr;
+      for (int r = jj + threadIdx.x; r < nr; r += NT) {
+        const double v = fabs(sp[r * SP_LD + jj]);
+        if (v > best) {
+          best = v;
+          besti = r;
+        }
+      }
+      block_argmax(best, besti, redv, redi);
+      const int pr = besti < nr ? besti : jj;  // all-NaN column (e.g. a pole energy): no interchange
+      if (threadIdx.x < SPW && pr != jj) {
+        const double t0 = sp[jj * SP_LD + threadIdx.x];
+        sp[jj * SP_LD + threadIdx.x] = sp[pr * SP_LD + threadIdx.x];
+        sp[pr * SP_LD + threadIdx.x] = t0;
+      }
+      if (threadIdx.x == 0) ipiv[s0 + jj] = c0 + pr;
+      __syncthreads();
+      const double piv = sp[jj * SP_LD + jj];
+      const bool zero = (piv == 0.0);
+      singular |= zero;
+      const double rpiv = zero ? 0.0 : 1.0 / piv;
+      double u[SPW];
+#pragma unroll
+      for (int q = 0; q < SPW; ++q) u[q] = sp[jj * SP_LD + q];
+      for (int r = jj + 1 + threadIdx.x; r < nr; r += NT) {
+        double *row = sp + r * SP_LD;
+        const double l = zero ? 0.0 : row[jj] * rpiv;
+        if (!zero) row[jj] = l;
+#pragma unroll
+        for (int q = 0; q < SPW; ++q)
+          if (q > jj) row[q] = fma(-l, u[q], row[q]);
+      }
+      __syncthreads();
+    }
+    // 3. write the factored sub-panel back
+    for (int q = threadIdx.x; q < nr * SPW; q += NT) {
+      const int r = q / SPW, c = q % SPW;
+      if (c < w) M[static_cast<int64_t>(c0 + r) * ld + c0 + c] = sp[r * SP_LD + c];
+    }
+    // 4. the sub-panel's interchanges, in order, on the rest of the augmented rows
+    for (int jj = 0; jj < w; ++jj) {
+      const int pr = ipiv[s0 + jj], j = c0 + jj;
+      if (pr != j) {
+        double *ra = M + static_cast<int64_t>(j) * ld;
+        double *rb = M + static_cast<int64_t>(pr) * ld;
+        constexpr int SU = 4;
+        for (int cb = sc0 + threadIdx.x; cb < sc1; cb += NT * SU) {
+          double va[SU], vb[SU];
+#pragma unroll
+          for (int q = 0; q < SU; ++q) {
+            const int c = cb + q * NT;
+            const bool ok = c < sc1 && (c < c0 || c >= c0 + w);
+            va[q] = ok ? ra[c] : 0.0;
+            vb[q] = ok ? rb[c] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < SU; ++q) {
+            const int c = cb + q * NT;
+            if (c < sc1 && (c < c0 || c >= c0 + w)) {
+              ra[c] = vb[q];
+              rb[c] = va[q];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // 5. rank-w update of the panel's remaining columns [c0+w, p0+bw)
+    const int cr0 = c0 + w, nc = p0 + bw - cr0;
+    if (nc > 0) {
+      // U rows c0..c0+w-1: unit-lower solve with L_ss (sp), one thread per column
+      if (threadIdx.x < nc) {
+        const int c = cr0 + threadIdx.x;
+        double x[SPW];
+#pragma unroll
+        for (int q = 0; q < SPW; ++q) {
+          double v = q < w ? M[static_cast<int64_t>(c0 + q) * ld + c] : 0.0;
+#pragma unroll
+          for (int k = 0; k < q; ++k) v = fma(-sp[q * SP_LD + k], x[k], v);
+          x[q] = v;
+        }
+#pragma unroll
+        for (int q = 0; q < SPW; ++q) {
+          ubuf[q * PB + threadIdx.x] = x[q];
+          if (q < w) M[static_cast<int64_t>(c0 + q) * ld + c] = x[q];
+        }
+      }
+      __syncthreads();
+      // rows c0+w..n-1: M[i][c] -= sum_q L[i][q] U[q][c]; warp per row, lane per column
+      constexpr int UNR = 8;
+      for (int r0 = w + warp; r0 < nr; r0 += NW * UNR) {
+        double x[UNR];
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const int r = r0 + q * NW;
+          x[q] = (r < nr && lane < nc) ? M[static_cast<int64_t>(c0 + r) * ld + cr0 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const int r = r0 + q * NW;
+          if (r < nr && lane < nc) {
+            double v = x[q];
+#pragma unroll
+            for (int k = 0; k < SPW; ++k) v = fma(-sp[r * SP_LD + k], ubuf[k * PB + lane], v);
+            M[static_cast<int64_t>(c0 + r) * ld + cr0 + lane] = v;
+          }
+        }
+      }
     }
   }
-  block_argmax(best, besti, redv, redi);
-  for (int jj = 0; jj < bw; ++jj) {
-    const int j = p0 + jj;
-    const int pr = besti < n ? besti : j;  // all-NaN column (e.g. a pole energy): no interchange
-    if (pr != j) {
-      double *a = M + static_cast<int64_t>(j) * ld;
-      double *b = M + static_cast<int64_t>(pr) * ld;
-      constexpr int SU = 4;
-      for (int c0 = sc0 + threadIdx.x; c0 < sc1; c0 += NT * SU) {
-        double va[SU], vb[SU];
-#pragma unroll
-        for (int q = 0; q < SU; ++q) {
-          const int c = c0 + q * NT;
-          if (c < sc1) {
-            va[q] = a[c];
-            vb[q] = b[c];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < SU; ++q) {
-          const int c = c0 + q * NT;
-          if (c < sc1) {
-            a[c] = vb[q];
-            b[c] = va[q];
-          }
-        }
-      }
-    }
-    if (threadIdx.x == 0) ipiv[jj] = pr;
-    __syncthreads();
-    const double u = lane < bw ? M[static_cast<int64_t>(j) * ld + p0 + lane] : 0.0;
-    const double piv = __shfl_sync(0xffffffffu, u, jj);
-    const bool zero = (piv == 0.0);
-    singular |= zero;
-    const double rpiv = zero ? 0.0 : 1.0 / piv;
-    best = -1.0;
-    besti = n;
-    const bool track = (jj + 1 < bw);
-    // rows j+1 .. n-1, warp-strided, UNR rows in flight per warp
-    constexpr int UNR = 8;
-    for (int i0 = j + 1 + warp; i0 < n; i0 += NW * UNR) {
-      double x[UNR];
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int i = i0 + q * NW;
-        x[q] = (i < n && lane < bw) ? M[static_cast<int64_t>(i) * ld + p0 + lane] : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int i = i0 + q * NW;
-        const double xj = __shfl_sync(0xffffffffu, x[q], jj);
-        const double l = xj * rpiv;
-        double y = x[q];
-        if (lane == jj)
-          y = zero ? xj : l;
-        else if (lane > jj)
-          y = fma(-l, u, y);
-        if (i < n && lane >= jj && lane < bw) M[static_cast<int64_t>(i) * ld + p0 + lane] = y;
-        if (track) {
-          const double v = fabs(__shfl_sync(0xffffffffu, y, jj + 1));
-          if (i < n && v > best) {
-            best = v;
-            besti = i;
-          }
-        }
-      }
-    }
-    if (track) block_argmax(best, besti, redv, redi);
-    __syncthreads();
-  }
+  __syncthreads();
   return singular;
 }
 

@@ -20,6 +20,7 @@ struct MatchSmem {
   double redv[NW];
   int redi[NW];
   int ipiv[NB];
+  double ubuf[SPW * PB];
   GemmSync gs;
 };
 
@@ -96,14 +97,15 @@ __global__ void __launch_bounds__(NT, 1)
     int singular = 0;
     for (int P0 = 0; P0 < n; P0 += NB) {
       const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
-      singular |= panel_lu(Mw, ldm, n, P0, w1, P0, ncols, sm.ipiv, sm.redv, sm.redi);
+      singular |= panel_lu(Mw, ldm, n, P0, w1, P0, ncols, sm.ipiv, sm.gemm, sm.ubuf, sm.redv, sm.redi);
       if (w2 > 0) {
         // right half of the outer block: U_ab = L_aa^{-1} A_ab (32 x 32); A_.b -= L_.a U_ab
         tri_inv64(Mw, ldm, P0, w1, TRI_UNIT_LOWER, sm.tri, Tv.base);
         gemm_set(w1, w2, w1, opk(Tv, 0, 0), opn(Mv, P0, P0 + w1), Mv, P0, P0 + w1, false, 0.0, smg, gs);
         gemm_sub(n - P0 - w1, w2, w1, opk(Mv, P0 + w1, P0), opn(Mv, P0, P0 + w1), Mv, P0 + w1,
                  P0 + w1, false, smg, gs);
-        singular |= panel_lu(Mw, ldm, n, P0 + w1, w2, P0, ncols, sm.ipiv + PB, sm.redv, sm.redi);
+        singular |= panel_lu(Mw, ldm, n, P0 + w1, w2, P0, ncols, sm.ipiv + PB, sm.gemm, sm.ubuf, sm.redv,
+                              sm.redi);
       }
       // trailing columns (A part and right-hand sides); when the last block ends on an odd n the
       // zero pad column n is skipped so that every C row stays 16-byte aligned

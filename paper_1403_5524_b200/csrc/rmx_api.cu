@@ -263,7 +263,9 @@ rmx_rc rmx_match_K(rmx_ctx *c, const double *R, const double *F, const double *G
   if (!c) return RMX_EINVAL;
   if (!R || !F || !G || !Fp || !Gp || !K) return fail(c, RMX_EINVAL, "rmx_match_K: null pointer");
   if (nch < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_match_K: sizes must be >= 1");
-  if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_match_K: nch too large");
+  if (nch > kMaxMatchChannels)
+    return fail(c, RMX_EINVAL, "rmx_match_K: nch > " + std::to_string(kMaxMatchChannels) +
+                                   " (smem-staged LU sub-panels)");
   if (!(a > 0.0)) return fail(c, RMX_EINVAL, "rmx_match_K: a must be > 0");
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
@@ -315,7 +317,9 @@ rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int
   if (!w || !Ek || !E || !F || !G || !Fp || !Gp || !rowsum)
     return fail(c, RMX_EINVAL, "rmx_sweep: null pointer");
   if (nch < 1 || nlev < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_sweep: sizes must be >= 1");
-  if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_sweep: nch too large");
+  if (nch > kMaxMatchChannels)
+    return fail(c, RMX_EINVAL, "rmx_sweep: nch > " + std::to_string(kMaxMatchChannels) +
+                                   " (smem-staged LU sub-panels)");
   if (!(a > 0.0)) return fail(c, RMX_EINVAL, "rmx_sweep: a must be > 0");
   if (ldw < nlev || (ldw & 1) || !aligned16(w))
     return fail(c, RMX_EINVAL, "rmx_sweep: ldw must be >= nlev and even, w 16-byte aligned");

@@ -69,6 +69,10 @@ cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t n
                         double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
                         int32_t *status, cudaStream_t st);
 
+// largest channel count the matching kernel supports: its LU sub-panels (n x 9 doubles) are
+// staged in the ~216 KB shared-memory union of the kernel
+constexpr int64_t kMaxMatchChannels = 2944;
+
 // box rows of the NVIEW tensor-map variants used by the CTA GEMM (cta_la.cuh)
 constexpr int kViewBoxRows[3] = {128, 64, 32};
 
