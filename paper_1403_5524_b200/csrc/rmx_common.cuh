@@ -41,6 +41,10 @@ __device__ __forceinline__ void lds128(double &x, double &y, uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
 }
 
+__device__ __forceinline__ void stg128(double *p, double x, double y) {
+  asm volatile("st.global.v2.f64 [%0], {%1,%2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
+}
+
 // ---- cp.async (LDGSTS) -------------------------------------------------------------------------
 // 16-byte async copy with zero fill of the bytes beyond src_bytes (0, 8 or 16).
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, int src_bytes) {
