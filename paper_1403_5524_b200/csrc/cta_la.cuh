@@ -24,7 +24,7 @@ constexpr int BM = 128, BN = 64, BK = 32, WM = 4, WN = 2;
 constexpr int WTM = BM / WM, WTN = BN / WN;  // 32 x 32 warp tile
 constexpr int MI = WTM / 8, NI = WTN / 8;    // 4 x 4 DMMA fragments
 constexpr int PB = 32;                        // inner panel / triangle width of the factorizations
-constexpr int NB = 2 * PB;                    // outer block width (K of the big trailing GEMMs)
+constexpr int NB = 4 * PB;                    // outer block width (K of the big trailing GEMMs)
 constexpr int STAGES = 3;                     // A/B ring depth
 // TMA boxes are 16 doubles (128 B, the SWIZZLE_128B span) wide:
 //   view 0: {16, 128} rows   k-contiguous A slices (2 boxes per BK = 32)
@@ -38,9 +38,11 @@ constexpr int C_ELEMS = BM * CS_LD;
 constexpr int GEMM_SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_ELEMS * 8;  // + 1024 alignment slack
 constexpr int GEMM_SMEM_DOUBLES = GEMM_SMEM_BYTES / 8;
 constexpr int TRI_LD = PB + 1;                // padded pitch of a bw x bw triangle in smem
-constexpr int TB = NB;                        // edge of the diagonal-block inverses (64)
+constexpr int TB = 64;                        // edge of the smem-computed triangular inverses
 constexpr int TB_LD = TB + 1;
-constexpr int TRI_SMEM_DOUBLES = 2 * TB * TB_LD;  // block + its inverse (aliases the gemm smem)
+constexpr int TG = NB;                        // edge (and pitch) of the global inverse Tg (128)
+constexpr int CH_LD = NB + 1;                 // pitch of the smem Cholesky block
+constexpr int TRI_SMEM_DOUBLES = (2 * TB * TB_LD > NB * CH_LD) ? 2 * TB * TB_LD : NB * CH_LD;
 
 // A matrix of a workspace slot: raw pointer + leading dimension, and its TMA descriptors
 // (NVIEW box shapes, see above; the tensor extent is the matrix allocation, out-of-range
@@ -373,8 +375,10 @@ __device__ __forceinline__ void gemm_set(int M, int N, int K, const Op &a, const
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 // C^T = A.B: element (i, j) of the product goes to the submatrix of `c` at (r0 + j, c0 + i).
-// Used to apply a 64 x 64 triangular inverse to a wide block (X = T X computed as X^T = X^T T^T,
-// so the long dimension runs over the 128-row tile side).
+// In-place use is safe when the operand being overwritten is B and M <= BM (one tile row): each
+// output tile then depends only on its own rows of B.
+// NOTE: any in-place GEMM must have its overwritten operand confined to one tile row / column;
+// otherwise a later tile would read values an earlier tile already stored.
 __device__ __forceinline__ void gemm_set_t(int M, int N, int K, const Op &a, const Op &b,
                                            const MatView &c, int cr0, int cc0, double *smem,
                                            GemmSync *gs) {
@@ -656,7 +660,7 @@ __device__ __forceinline__ int chol_diag(double *S, int64_t ld, int p0, int bw, 
 //   lower:  [[A, 0], [C, B]]^-1 = [[A^-1, 0], [-B^-1 C A^-1, B^-1]]
 //   upper:  [[A, C], [0, B]]^-1 = [[A^-1, -A^-1 C B^-1], [0, B^-1]]
 __device__ __forceinline__ void tri_inv64(const double *src, int64_t ld, int p0, int W, int kind,
-                                          double *sm, double *Tg) {
+                                          double *sm, double *Tg, int ldt = TB) {
   double *Lb = sm, *Tb = sm + TB * TB_LD;
   __syncthreads();
   for (int q = threadIdx.x; q < TB * TB; q += NT) {
@@ -731,46 +735,76 @@ __device__ __forceinline__ void tri_inv64(const double *src, int64_t ld, int p0,
       const bool zero = upper ? (r >= 32 && c < 32) : (r < 32 && c >= 32);
       v = off ? Lb[r * TB_LD + c] : (zero ? 0.0 : Tb[r * TB_LD + c]);
     }
-    Tg[q] = v;
+    Tg[r * ldt + c] = v;
   }
   __syncthreads();
 }
 
-// Unblocked Cholesky of the W x W (W <= 64) diagonal block S[p0.., p0..] (lower) in shared
+// Unblocked Cholesky of the W x W (W <= NB) diagonal block S[p0.., p0..] (lower) in shared
 // memory, written back to S. Returns 1 if a non-positive pivot appears (S = I + K K^T is SPD).
-__device__ __forceinline__ int chol_diag64(double *S, int64_t ld, int p0, int W, double *sm) {
+__device__ __forceinline__ int chol_diag_blk(double *S, int64_t ld, int p0, int W, double *sm) {
   double *Lb = sm;
   __shared__ int bad64;
   __syncthreads();
   if (threadIdx.x == 0) bad64 = 0;
   for (int q = threadIdx.x; q < W * W; q += NT) {
     const int r = q / W, c = q % W;
-    Lb[r * TB_LD + c] = c <= r ? S[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
+    Lb[r * CH_LD + c] = c <= r ? S[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
   }
   __syncthreads();
   for (int c = 0; c < W; ++c) {
-    const double d2 = Lb[c * TB_LD + c];
+    const double d2 = Lb[c * CH_LD + c];
     const double d = sqrt(d2);
     __syncthreads();  // everyone has read the pivot before it is overwritten
     if (threadIdx.x == 0) {
       if (!(d2 > 0.0)) bad64 = 1;
-      Lb[c * TB_LD + c] = d;
+      Lb[c * CH_LD + c] = d;
     }
-    for (int r = c + 1 + threadIdx.x; r < W; r += NT) Lb[r * TB_LD + c] /= d;
+    for (int r = c + 1 + threadIdx.x; r < W; r += NT) Lb[r * CH_LD + c] /= d;
     __syncthreads();
     const int m = W - c - 1;  // trailing block rows/cols c+1..W-1, lower part
     for (int q = threadIdx.x; q < m * m; q += NT) {
       const int r = c + 1 + q / m, k = c + 1 + q % m;
-      if (k <= r) Lb[r * TB_LD + k] = fma(-Lb[r * TB_LD + c], Lb[k * TB_LD + c], Lb[r * TB_LD + k]);
+      if (k <= r) Lb[r * CH_LD + k] = fma(-Lb[r * CH_LD + c], Lb[k * CH_LD + c], Lb[r * CH_LD + k]);
     }
     __syncthreads();
   }
   for (int q = threadIdx.x; q < W * W; q += NT) {
     const int r = q / W, c = q % W;
-    if (c <= r) S[static_cast<int64_t>(p0 + r) * ld + p0 + c] = Lb[r * TB_LD + c];
+    if (c <= r) S[static_cast<int64_t>(p0 + r) * ld + p0 + c] = Lb[r * CH_LD + c];
   }
   __syncthreads();
   return bad64;
+}
+
+
+// Inverse of the W x W (W <= NB = 128) triangular diagonal block of `sv` at (p0, p0) into the
+// global Tg [128][128] (view tv, zero outside W x W): 64 x 64 diagonal inverses in shared memory
+// (tri_inv64) and the off-diagonal 64-block by two DMMA GEMMs with the 2 x 2 block formula
+//   lower: T21 = -T2 (L21 T1)          upper: T12 = -T1 (U12 T2)
+// (the product is staged in the quadrant that ends up zero, then cleared).
+__device__ __forceinline__ void tri_inv128(const MatView &sv, int p0, int W, int kind,
+                                           const MatView &tv, double *smem, GemmSync *gs) {
+  double *Tg = tv.base;
+  __syncthreads();
+  for (int q = threadIdx.x; q < TG * TG; q += NT) Tg[q] = 0.0;
+  const int W1 = min(W, TB), W2 = W - W1;
+  tri_inv64(sv.base, sv.ld, p0, W1, kind, smem, Tg, TG);
+  if (W2 > 0) {
+    tri_inv64(sv.base, sv.ld, p0 + TB, W2, kind, smem, Tg + TB * TG + TB, TG);
+    if (kind != TRI_UPPER) {
+      // P = L21 T1 -> Tg[0:W2, 64:128); T21 = -T2 P -> Tg[64:64+W2, 0:64)
+      gemm_set(W2, TB, TB, opk(sv, p0 + TB, p0), opn(tv, 0, 0), tv, 0, TB, false, 0.0, smem, gs);
+      gemm_sub(W2, TB, W2, opk(tv, TB, TB), opn(tv, 0, TB), tv, TB, 0, false, smem, gs);
+      for (int q = threadIdx.x; q < TB * TB; q += NT) Tg[(q / TB) * TG + TB + (q % TB)] = 0.0;
+    } else {
+      // P = U12 T2 -> Tg[64:128, 0:W2); T12 = -T1 P -> Tg[0:64, 64:64+W2)
+      gemm_set(TB, W2, W2, opk(sv, p0, p0 + TB), opn(tv, TB, TB), tv, TB, 0, false, 0.0, smem, gs);
+      gemm_sub(TB, W2, TB, opk(tv, 0, 0), opn(tv, TB, 0), tv, 0, TB, false, smem, gs);
+      for (int q = threadIdx.x; q < TB * TB; q += NT) Tg[(TB + q / TB) * TG + (q % TB)] = 0.0;
+    }
+  }
+  __syncthreads();
 }
 
 }  // namespace la

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int ldm = static_cast<int>(L.ldm), npad = static_cast<int>(L.npad);
   double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
   const MatView Mv{views + (blockIdx.x * 2 + 0) * NVIEW, slot + L.m_off, ldm};
-  const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, TB};
+  const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, TG};
   double *Mw = Mv.base;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
@@ -90,32 +90,34 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
 
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
-    // Outer blocks of W = 64 columns: two 32-wide panels (the second after a K = 32 update), then
-    // U12 = L11^{-1} A12 as ONE DMMA GEMM with the explicit 64 x 64 inverse (computed transposed,
-    // U12^T = A12^T L11^{-T}, so the long trailing dimension runs along the 128-row tiles), then the
-    // K = 64 trailing update. Every operand stays in the slot workspace (aligned, even pitch).
+    // Outer blocks of W = NB = 128 columns, factored as four 32-wide panels (each followed by a
+    // K = 32 update of the block's remaining columns), then U12 = L11^{-1} A12 as ONE in-place DMMA
+    // GEMM with the explicit 128 x 128 inverse (one 128-row tile row), then the K = 128 trailing
+    // update.
     int singular = 0;
     for (int P0 = 0; P0 < n; P0 += NB) {
-      const int W = min(NB, n - P0), w1 = min(PB, W), w2 = W - w1;
-      singular |= panel_lu(Mw, ldm, n, P0, w1, P0, ncols, sm.ipiv, sm.gemm, sm.ubuf, sm.redv, sm.redi);
-      if (w2 > 0) {
-        // right half of the outer block: U_ab = L_aa^{-1} A_ab (32 x 32); A_.b -= L_.a U_ab
-        tri_inv64(Mw, ldm, P0, w1, TRI_UNIT_LOWER, sm.tri, Tv.base);
-        gemm_set(w1, w2, w1, opk(Tv, 0, 0), opn(Mv, P0, P0 + w1), Mv, P0, P0 + w1, false, 0.0, smg, gs);
-        gemm_sub(n - P0 - w1, w2, w1, opk(Mv, P0 + w1, P0), opn(Mv, P0, P0 + w1), Mv, P0 + w1,
-                 P0 + w1, false, smg, gs);
-        singular |= panel_lu(Mw, ldm, n, P0 + w1, w2, P0, ncols, sm.ipiv + PB, sm.gemm, sm.ubuf, sm.redv,
-                              sm.redi);
+      const int W = min(NB, n - P0);
+      for (int q0 = 0; q0 < W; q0 += PB) {
+        const int c = P0 + q0, wq = min(PB, W - q0), rem = W - q0 - wq;
+        singular |= panel_lu(Mw, ldm, n, c, wq, P0, ncols, sm.ipiv + q0, sm.gemm, sm.ubuf, sm.redv,
+                             sm.redi);
+        if (rem > 0) {
+          // block columns right of this panel: U rows = L_qq^{-1} A ; rows below -= L U
+          tri_inv64(Mw, ldm, c, wq, TRI_UNIT_LOWER, sm.tri, Tv.base, TG);
+          gemm_set(wq, rem, wq, opk(Tv, 0, 0), opn(Mv, c, c + wq), Mv, c, c + wq, false, 0.0, smg, gs);
+          gemm_sub(n - c - wq, rem, wq, opk(Mv, c + wq, c), opn(Mv, c, c + wq), Mv, c + wq, c + wq,
+                   false, smg, gs);
+        }
       }
       // trailing columns (A part and right-hand sides); when the last block ends on an odd n the
       // zero pad column n is skipped so that every C row stays 16-byte aligned
       const int ct = min((P0 + W + 1) & ~1, ncols);
       const int nt = ncols - ct;
       if (nt > 0) {
-        tri_inv64(Mw, ldm, P0, W, TRI_UNIT_LOWER, sm.tri, Tv.base);  // L11^{-1}
-        // U12^T = A12^T L11^{-T}: A'(j, k) = M[P0+k][ct+j], B'(i, k) = Tg[i][k]; stored transposed
-        gemm_set_t(nt, W, W, opn(Mv, P0, ct), opk(Tv, 0, 0), Mv, P0, ct, smg, gs);
-        // trailing update with K = W
+        tri_inv128(Mv, P0, W, TRI_UNIT_LOWER, Tv, smg, gs);  // L11^{-1}
+        // U12 = L11^{-1} A12 in place: W <= 128 = BM rows, so each output tile column depends only
+        // on its own input columns
+        gemm_set(W, nt, W, opk(Tv, 0, 0), opn(Mv, P0, ct), Mv, P0, ct, false, 0.0, smg, gs);
         if (P0 + W < n)
           gemm_sub(n - P0 - W, nt, W, opk(Mv, P0 + W, P0), opn(Mv, P0, ct), Mv, P0 + W, ct, false,
                    smg, gs);
@@ -126,8 +128,8 @@ __global__ void __launch_bounds__(NT, 1)
     if (o > 0) {
       for (int P0 = ((n - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
         const int W = min(NB, n - P0);
-        tri_inv64(Mw, ldm, P0, W, TRI_UPPER, sm.tri, Tv.base);  // U_pp^{-1}
-        gemm_set_t(o, W, W, opn(Mv, P0, npad), opk(Tv, 0, 0), Mv, P0, npad, smg, gs);
+        tri_inv128(Mv, P0, W, TRI_UPPER, Tv, smg, gs);  // U_pp^{-1}
+        gemm_set(W, o, W, opk(Tv, 0, 0), opn(Mv, P0, npad), Mv, P0, npad, false, 0.0, smg, gs);
         if (P0 > 0)
           gemm_sub(P0, o, W, opk(Mv, 0, P0), opn(Mv, P0, npad), Mv, 0, npad, false, smg, gs);
       }
@@ -165,7 +167,7 @@ int64_t match_ws_doubles_per_slot(int64_t nch) { return match_layout(nch).slot; 
 // Matrices of one slot whose TMA descriptors the kernel uses: (M, Tg), NVIEW box shapes each.
 void match_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
   const MatchLayout L = match_layout(nch);
-  specs = {MatSpec{L.m_off, nch, L.ldm, L.ldm}, MatSpec{L.tg_off, TB, TB, TB}};
+  specs = {MatSpec{L.m_off, nch, L.ldm, L.ldm}, MatSpec{L.tg_off, TG, TG, TG}};
 }
 
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,

@@ -29,7 +29,7 @@ __host__ __device__ inline MatchLayout match_layout(int64_t nch) {
   L.ldm = 2 * L.npad;  // [A | pad | B_open]
   L.m_off = 0;
   L.tg_off = nch * L.ldm + 32;
-  L.slot = L.tg_off + 64 * 64 + 32;  // Tg: inverse of a 64 x 64 diagonal block
+  L.slot = L.tg_off + 128 * 128 + 32;  // Tg: inverse of a 128 x 128 diagonal block
   return L;
 }
 __host__ __device__ inline TepiLayout tepi_layout(int64_t nch) {
@@ -39,7 +39,7 @@ __host__ __device__ inline TepiLayout tepi_layout(int64_t nch) {
   L.x_off = nch * L.ldo + 32;
   L.k_off = L.x_off + nch * L.ldo + 32;
   L.tg_off = L.k_off + nch * L.ldo + 32;
-  L.slot = L.tg_off + 64 * 64 + 32;
+  L.slot = L.tg_off + 128 * 128 + 32;
   return L;
 }
 

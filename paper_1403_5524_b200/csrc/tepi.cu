@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(NT, 1)
   const MatView Sv{vw + 0 * NVIEW, slot + L.s_off, ldo};
   const MatView Xv{vw + 1 * NVIEW, slot + L.x_off, ldo};
   const MatView Kv{vw + 2 * NVIEW, slot + L.k_off, ldo};
-  const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, TB};
-  double *S = Sv.base, *Tg = Tv.base;
+  const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, TG};
+  double *S = Sv.base;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
 
@@ -105,33 +105,34 @@ __global__ void __launch_bounds__(NT, 1)
       __syncthreads();
       // S = I + K_oo K_oo^T (lower tiles)
       gemm_set(o, o, o, opk(Kv, 0, 0), opk(Kv, 0, 0), Sv, 0, 0, true, 1.0, smg, gs);
-      // blocked Cholesky S = L L^T (lower), 64-wide blocks: diagonal block in smem, then
-      // L21 = S21 L11^{-T} as one in-place GEMM with the explicit inverse, then the K = 64 update
+      // blocked Cholesky S = L L^T (lower), 128-wide blocks: diagonal block in smem, then
+      // L21 = S21 L11^{-T} as one in-place GEMM with the explicit inverse, then the K = 128 update
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0);
-        bad |= chol_diag64(S, ldo, P0, W, sm.tri);
+        bad |= chol_diag_blk(S, ldo, P0, W, sm.tri);
         if (P0 + W < o) {
-          tri_inv64(S, ldo, P0, W, TRI_LOWER, sm.tri, Tg);
-          gemm_set(o - P0 - W, W, W, opk(Sv, P0 + W, P0), opk(Tv, 0, 0), Sv, P0 + W, P0, false, 0.0,
-                   smg, gs);
+          tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
+          // L21^T = L11^{-1} S21^T (stored transposed, in place): one 128-row tile row, so each
+          // output tile depends only on its own rows of S21
+          gemm_set_t(W, o - P0 - W, W, opk(Tv, 0, 0), opk(Sv, P0 + W, P0), Sv, P0 + W, P0, smg, gs);
           const int m2 = o - P0 - W;
           gemm_sub(m2, m2, W, opk(Sv, P0 + W, P0), opk(Sv, P0 + W, P0), Sv, P0 + W, P0 + W, true,
                    smg, gs);
         }
       }
-      // forward: L Z = K  (X holds K_oo); X_p = L_pp^{-1} X_p as X_p^T = X_p^T L_pp^{-T}
+      // forward: L Z = K  (X holds K_oo); X_p = L_pp^{-1} X_p (in place, one 128-row tile row)
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0);
-        tri_inv64(S, ldo, P0, W, TRI_LOWER, sm.tri, Tg);
-        gemm_set_t(o, W, W, opn(Xv, P0, 0), opk(Tv, 0, 0), Xv, P0, 0, smg, gs);
+        tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
+        gemm_set(W, o, W, opk(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
         if (P0 + W < o)
           gemm_sub(o - P0 - W, o, W, opk(Sv, P0 + W, P0), opn(Xv, P0, 0), Xv, P0 + W, 0, false, smg, gs);
       }
-      // backward: L^T X = Z; X_p = L_pp^{-T} X_p as X_p^T = X_p^T L_pp^{-1}: B'(i, k) = Tg[k][i]
+      // backward: L^T X = Z; X_p = L_pp^{-T} X_p: A(i, k) = Tg[k][i]
       for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
         const int W = min(NB, o - P0);
-        tri_inv64(S, ldo, P0, W, TRI_LOWER, sm.tri, Tg);
-        gemm_set_t(o, W, W, opn(Xv, P0, 0), opn(Tv, 0, 0), Xv, P0, 0, smg, gs);
+        tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
+        gemm_set(W, o, W, opn(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
         if (P0 > 0)
           // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]
           gemm_sub(P0, o, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
@@ -180,7 +181,7 @@ int64_t tepi_ws_doubles_per_slot(int64_t nch) { return tepi_layout(nch).slot; }
 void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
   const TepiLayout L = tepi_layout(nch);
   specs = {MatSpec{L.s_off, nch, L.ldo, L.ldo}, MatSpec{L.x_off, nch, L.ldo, L.ldo},
-           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, TB, TB, TB}};
+           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, TG, TG, TG}};
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
