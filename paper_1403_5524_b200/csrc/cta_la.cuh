@@ -109,7 +109,10 @@ struct GemmArgs {
 // g maps to smem row (g>>1) + 4(g&1) so those reads are bank-conflict free under the swizzle.
 // Partial k-slices are masked (both operands zeroed beyond K).
 template <bool A_KC, bool B_KC>
-static __device__ __noinline__ void gemm_impl(const GemmArgs &ga, uint8_t *smem_al, GemmSync *gs) {
+static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem_al, GemmSync *gs) {
+  // argument block copied to registers once (it arrives by reference through the call ABI, i.e.
+  // from local memory; re-reading it in the epilogue cost long-scoreboard stalls)
+  const GemmArgs ga = gar;
   const int M = ga.M, N = ga.N, K = ga.K;
   const bool lower = ga.lower, readC = ga.read_c;
   __syncthreads();
