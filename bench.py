@@ -39,6 +39,26 @@ FP64_DMMA_PEAK_TFLOPS = 37.1
 FP64_DFMA_PEAK_TFLOPS = 34.2
 
 
+def ncu_traffic(workload: str, batch: int):
+    """DRAM bytes (read + write) per launch of the R kernel from the newest committed full ncu
+    capture (profiles/rNN_ncu_kernels.json, written by tools/summarize_profiles.py), when that
+    capture was taken on the same workload and energies per launch; else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_kernels.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        for name, ent in d.items():
+            if "rform" not in name:
+                continue
+            wl = ent.get("workload", {})
+            rd, wr = ent.get("dram__bytes_read.bytes"), ent.get("dram__bytes_write.bytes")
+            if wl.get("config") == workload and wl.get("energies_per_launch") == batch and rd and wr:
+                return rd + wr, os.path.basename(path)
+    return None, None
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -334,6 +354,7 @@ def main():
                          f"{dt:.1f} s, OpenMP over rows/energies"}
 
     if rank == 0:
+        traffic, traffic_src = ncu_traffic(args.config, batch)
         line = {
             "metric": "energies/sec (R->K->|T|^2 sweep)",
             "value": value, "unit": "energies/s", "n_gpus": world, "steps": args.steps,
@@ -347,7 +368,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "rform (FP64 DMMA R formation)",
                          "achieved": achieved_r, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,
-                         "traffic": None,
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": "measured FP64 DMMA.8x8x4 peak, tools/fp64_peak.cu on this pool "
                                         "(profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry",
                          "algorithmic": "nch(nch+1)*nlev flops per energy x energies per launch"},
