@@ -17,21 +17,21 @@
 
 namespace rmx {
 
-template <int BM_, int WM_, int WN_, int STAGES_>
+template <int BM_, int STAGES_>
 struct RformCfg {
-  static constexpr int BM = BM_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BM = BM_, STAGES = STAGES_;
   static constexpr int BK = 32;    // k per pipeline stage
   static constexpr int BOXK = 16;  // doubles per TMA box row (128 B = swizzle span)
-  static constexpr int NCW = WM * WN;
+  static constexpr int NB = BM / 32;                       // 32 x 32 blocks per tile dimension
+  static constexpr int NCW = (NB * NB / 2 > 4) ? NB * NB / 2 : 4;  // consumer warps, <= 2 blocks each
   static constexpr int NT = (NCW + 1) * 32;
-  static constexpr int WTM = BM / WM, WTN = BM / WN;
-  static constexpr int MI = WTM / 8, NI = WTN / 8;
   static constexpr int BOX_BYTES = BM * BOXK * 8;
   static constexpr int OP_BYTES = 2 * BOX_BYTES;   // one operand, one stage
   static constexpr int STAGE_BYTES = 2 * OP_BYTES;  // tile I + tile J
   static constexpr int SMEM_BYTES =
       1024 + STAGES * STAGE_BYTES + STAGES * BK * 8 + 2 * STAGES * 8 + 16;
   static_assert(BOX_BYTES % 1024 == 0, "swizzle-128B boxes must stay 1024-byte aligned");
+  static_assert(NB * NB <= 2 * NCW, "at most two 32x32 blocks per consumer warp");
 };
 
 __device__ __forceinline__ int frag_row_perm(int g) { return (g >> 1) + 4 * (g & 1); }
@@ -46,10 +46,172 @@ __device__ __forceinline__ void decode_pair(int p, int ntiles, int &ti, int &tj)
   tj = ti + p;
 }
 
+// Work split inside a tile: the useful 32x32 blocks (inside nch, and c >= r on a diagonal tile) of
+// each block row are cut into chunks of two adjacent blocks (one 32 x 64 warp tile, A fragments
+// shared) plus a single block when the row count is odd. Chunks are listed pairs first, then
+// singles, and dealt snake-wise to the four SM sub-partitions (warp w runs on sub-partition w % 4):
+// chunk i -> warp i for i < 4, warp 11 - i for i >= 4. A full tile (8 pairs) keeps the plain 4 x 2
+// warp grid; a diagonal tile (4 pairs + 2 singles) or a ragged edge tile costs the largest
+// sub-partition load (3 of 4 blocks) instead of a full tile. With NCW == 4 (64-row tiles) every
+// chunk is a single block. Returns the number of blocks (0, 1, 2) of this warp's chunk at (r, c).
+template <int NB, int NCW>
+__device__ __forceinline__ int rform_chunk(int warp, int rbm, int cbm, bool diag, int &r, int &c) {
+  constexpr bool PAIRS = NCW >= 8;
+  const int want = PAIRS ? ((warp < 4) ? warp : 11 - warp) : warp;
+  int idx = 0;
+  r = c = 0;
+  if (PAIRS) {
+    for (int rr = 0; rr < rbm; ++rr)
+      for (int cc = diag ? rr : 0; cc + 1 < cbm; cc += 2, ++idx)
+        if (idx == want) { r = rr; c = cc; return 2; }
+  }
+  for (int rr = 0; rr < rbm; ++rr) {
+    const int c0 = diag ? rr : 0;
+    for (int cc = PAIRS ? (((cbm - c0) & 1) ? cbm - 1 : cbm) : c0; cc < cbm; ++cc, ++idx)
+      if (idx == want) { r = rr; c = cc; return 1; }
+  }
+  return 0;
+}
+
+// One k-slab of DMMA for a warp owning block(s) of 32x32.
+//   MODE 0: two adjacent blocks of one block row (A fragments shared, 4 x 8 fragments, 64 DMMA / kk)
+//   MODE 2: one block (4 x 4 fragments, 32 DMMA / kk)
+template <int MODE>
+__device__ __forceinline__ void rform_slab(double (&acc)[2][4][4][2], uint32_t abase, uint32_t bbase,
+                                           uint32_t dbase, int box_bytes, const uint32_t (&arow)[2],
+                                           const uint32_t (&brow)[2], int t, int prow) {
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      // this lane's two k values: k = kb*16 + kk*8 + 2t + {0,1}; 16-byte chunk c = kk*4 + t
+      const uint32_t chunk = static_cast<uint32_t>(((kk * 4 + t) ^ prow) << 4);
+      double d0, d1;
+      lds128(d0, d1, dbase + (kb * 16 + kk * 8 + 2 * t) * 8);
+      if (MODE == 0) {
+        // two blocks of one block row: A fragments shared (4 A + 8 B fragments, 64 DMMA)
+        double a[4][2], b[2][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          lds128(a[mi][0], a[mi][1], abase + kb * box_bytes + arow[0] + mi * 1024 + chunk);
+          a[mi][0] *= d0;
+          a[mi][1] *= d1;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+            lds128(b[u][ni][0], b[u][ni][1], bbase + kb * box_bytes + brow[u] + ni * 1024 + chunk);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni)
+                dmma(acc[u][mi][ni][0], acc[u][mi][ni][1], a[mi][h], b[u][ni][h]);
+      } else {
+        // one block, or two blocks of different block rows done one after the other (keeps the
+        // live fragment set at 4 A + 4 B)
+#pragma unroll
+        for (int u = 0; u < (MODE == 1 ? 2 : 1); ++u) {
+          double a[4][2], b[4][2];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            lds128(a[mi][0], a[mi][1], abase + kb * box_bytes + arow[u] + mi * 1024 + chunk);
+            a[mi][0] *= d0;
+            a[mi][1] *= d1;
+          }
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+            lds128(b[ni][0], b[ni][1], bbase + kb * box_bytes + brow[u] + ni * 1024 + chunk);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni)
+                dmma(acc[u][mi][ni][0], acc[u][mi][ni][1], a[mi][h], b[ni][h]);
+        }
+      }
+    }
+  }
+}
+
+// One consumer warp: its chunk's k loop and epilogue (MODE 0: two blocks (r, c), (r, c + 1);
+// MODE 2: one block; MODE 3: no block, only releases the stages). Templated whole so that each
+// mode's accumulators get their own register allocation.
+template <class C, int MODE>
+__device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag, int rb0, int cb0,
+                                               int ti, int tj, int nch, int64_t e, int pair,
+                                               double inv2a, double *__restrict__ R,
+                                               int32_t *__restrict__ status) {
+  double *dsm = reinterpret_cast<double *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
+  uint64_t *empty = full + C::STAGES;
+  const int *pole_flag = reinterpret_cast<const int *>(empty + C::STAGES);
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int prow = frag_row_perm(g);
+  constexpr int NBLK = MODE == 0 ? 2 : (MODE == 2 ? 1 : 0);
+  double acc[2][4][4][2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[u][mi][ni][0] = acc[u][mi][ni][1] = 0.0;
+  // byte offsets of this lane's fragment rows inside a box (row * 128); swizzle xor = prow
+  // (fragment mi / ni of a block sits 8 rows = 1024 bytes further)
+  const uint32_t arow[2] = {static_cast<uint32_t>((rb0 * 32 + prow) * 128), 0u};
+  const uint32_t brow[2] = {static_cast<uint32_t>((cb0 * 32 + prow) * 128),
+                            static_cast<uint32_t>((cb0 * 32 + 32 + prow) * 128)};
+
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % C::STAGES;
+    mbar_wait(&full[s], (kt / C::STAGES) & 1);
+    if (MODE != 3) {
+      const uint32_t abase = smem_u32(smem + s * C::STAGE_BYTES);
+      const uint32_t bbase = diag ? abase : abase + C::OP_BYTES;
+      const uint32_t dbase = smem_u32(dsm + s * C::BK);
+      rform_slab<MODE>(acc, abase, bbase, dbase, C::BOX_BYTES, arow, brow, t, prow);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ===================== epilogue: scale, store tile + mirror =====================
+  const bool pole = (*reinterpret_cast<const volatile int *>(pole_flag)) != 0;
+  if (pole && pair == 0 && threadIdx.x == 0) set_status(status, e, RMX_E_POLE);
+  double *Re = R + e * static_cast<int64_t>(nch) * nch;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+#pragma unroll
+  for (int u = 0; u < NBLK; ++u) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int row = ti * C::BM + rb0 * 32 + mi * 8 + prow;
+      if (row >= nch) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = tj * C::BM + (cb0 + u) * 32 + ni * 8 + t + 4 * h;
+          if (col >= nch) continue;
+          if (diag && row > col) continue;  // lower half of a diagonal tile comes from its mirror
+          const double v = pole ? nan : acc[u][mi][ni][h] * inv2a;
+          Re[static_cast<int64_t>(row) * nch + col] = v;
+          if (row != col) Re[static_cast<int64_t>(col) * nch + row] = v;
+        }
+      }
+    }
+  }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1)
     rform_dmma_kernel(const __grid_constant__ CUtensorMap wmap, const double *__restrict__ Ek,
-                      const double *__restrict__ E, int nch, int nlev, int ntiles, int npairs,
+                      const double *__restrict__ E, int nch, int nlev, int ntiles, int nen,
                       double inv2a, double *__restrict__ R, int32_t *__restrict__ status) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -59,8 +221,11 @@ __global__ void __launch_bounds__(C::NT, 1)
   uint64_t *empty = full + C::STAGES;
   int *pole_flag = reinterpret_cast<int *>(empty + C::STAGES);
 
-  const int pair = blockIdx.x % npairs;
-  const int64_t e = blockIdx.x / npairs;
+  // energies fastest: the CTAs resident at any moment are (mostly) one tile pair for up to ~148
+  // energies, so they stream the same two 128-row slabs of W in lock step and W is fetched from
+  // HBM about once per wave (whole-W working set per wave otherwise: DRAM ~1.3 TB/launch).
+  const int pair = blockIdx.x / nen;
+  const int64_t e = blockIdx.x % nen;
   int ti, tj;
   decode_pair(pair, ntiles, ti, tj);
   const bool diag = (ti == tj);
@@ -113,81 +278,16 @@ __global__ void __launch_bounds__(C::NT, 1)
   }
 
   // ===================== consumer warps: FP64 DMMA =====================
-  const int wm = warp % C::WM, wn = warp / C::WM;
-  const int g = lane >> 2, t = lane & 3;
-  const int prow = frag_row_perm(g);
-  double acc[C::MI][C::NI][2];
-#pragma unroll
-  for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-
-  // byte offsets of this lane's fragment rows inside a box (row * 128); swizzle xor = prow
-  uint32_t arow[C::MI], brow[C::NI];
-#pragma unroll
-  for (int mi = 0; mi < C::MI; ++mi) arow[mi] = (wm * C::WTM + mi * 8 + prow) * 128;
-#pragma unroll
-  for (int ni = 0; ni < C::NI; ++ni) brow[ni] = (wn * C::WTN + ni * 8 + prow) * 128;
-
-  for (int kt = 0; kt < nk; ++kt) {
-    const int s = kt % C::STAGES;
-    mbar_wait(&full[s], (kt / C::STAGES) & 1);
-    const uint32_t abase = smem_u32(smem + s * C::STAGE_BYTES);
-    const uint32_t bbase = diag ? abase : abase + C::OP_BYTES;
-    const uint32_t dbase = smem_u32(dsm + s * C::BK);
-#pragma unroll
-    for (int kb = 0; kb < 2; ++kb) {
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        // this lane's two k values: k = kb*16 + kk*8 + 2t + {0,1}; 16-byte chunk c = kk*4 + t
-        const uint32_t chunk = static_cast<uint32_t>(((kk * 4 + t) ^ prow) << 4);
-        double d0, d1;
-        lds128(d0, d1, dbase + (kb * 16 + kk * 8 + 2 * t) * 8);
-        double a[C::MI][2], b[C::NI][2];
-#pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi) {
-          lds128(a[mi][0], a[mi][1], abase + kb * C::BOX_BYTES + arow[mi] + chunk);
-          a[mi][0] *= d0;
-          a[mi][1] *= d1;
-        }
-#pragma unroll
-        for (int ni = 0; ni < C::NI; ++ni)
-          lds128(b[ni][0], b[ni][1], bbase + kb * C::BOX_BYTES + brow[ni] + chunk);
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < C::NI; ++ni)
-              dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi][h], b[ni][h]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-
-  // ===================== epilogue: scale, store tile + mirror =====================
-  const bool pole = (*reinterpret_cast<volatile int *>(pole_flag)) != 0;
-  if (pole && pair == 0 && warp == 0 && lane == 0) set_status(status, e, RMX_E_POLE);
-  double *Re = R + e * static_cast<int64_t>(nch) * nch;
-  const double nan = __longlong_as_double(0x7ff8000000000000LL);
-#pragma unroll
-  for (int mi = 0; mi < C::MI; ++mi) {
-    const int row = ti * C::BM + wm * C::WTM + mi * 8 + prow;
-    if (row >= nch) continue;
-#pragma unroll
-    for (int ni = 0; ni < C::NI; ++ni) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = tj * C::BM + wn * C::WTN + ni * 8 + t + 4 * h;
-        if (col >= nch) continue;
-        if (diag && row > col) continue;  // lower half of a diagonal tile comes from its mirror
-        const double v = pole ? nan : acc[mi][ni][h] * inv2a;
-        Re[static_cast<int64_t>(row) * nch + col] = v;
-        if (row != col) Re[static_cast<int64_t>(col) * nch + row] = v;
-      }
-    }
-  }
+  const int rbm = min(C::NB, (nch - ti * C::BM + 31) / 32);
+  const int cbm = min(C::NB, (nch - tj * C::BM + 31) / 32);
+  int rb0, cb0;
+  const int nblk = rform_chunk<C::NB, C::NCW>(warp, rbm, cbm, diag, rb0, cb0);
+  if (nblk == 2)
+    rform_consumer<C, 0>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status);
+  else if (nblk == 1)
+    rform_consumer<C, 2>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status);
+  else
+    rform_consumer<C, 3>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status);
 }
 
 // Small-channel path (nch <= 32, e.g. BASELINE.json:7 'tiny'): one CTA per energy, each thread owns
@@ -339,7 +439,7 @@ static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *
   for (int64_t e0 = 0; e0 < ne; e0 += max_e) {
     const int64_t n = (ne - e0 < max_e) ? ne - e0 : max_e;
     rform_dmma_kernel<C><<<static_cast<unsigned>(n * npairs), C::NT, C::SMEM_BYTES, st>>>(
-        map, Ek, E + e0, nch, nlev, ntiles, npairs, inv2a,
+        map, Ek, E + e0, nch, nlev, ntiles, static_cast<int>(n), inv2a,
         R + e0 * static_cast<int64_t>(nch) * nch, status ? status + e0 : nullptr);
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return ce;
@@ -347,8 +447,8 @@ static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *
   return cudaSuccess;
 }
 
-using Rform128 = RformCfg<128, 4, 2, 3>;
-using Rform64 = RformCfg<64, 2, 2, 3>;
+using Rform128 = RformCfg<128, 3>;
+using Rform64 = RformCfg<64, 3>;
 
 int rform_tile_for(int64_t nch) {
   if (nch <= 32) return 0;
