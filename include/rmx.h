@@ -119,6 +119,32 @@ rmx_rc rmx_collision_strength(rmx_ctx *ctx, const double *K, int64_t nch, int64_
                               int32_t *status);
 
 /*
+ * rmx_collision_strength_levels - NEXT-2 of SURVEY.md §8(f) ("each block
+ * represents a partial wave ... reduced to the time required for a single partial wave"):
+ * level-pair collision strengths of one symmetry (partial wave), accumulated with weight g:
+ *
+ *     omega[e][a][b] += g * sum_{i in level a} sum_{j in level b} |T_ij(E_e)|^2
+ *
+ * for every pair of OPEN levels (a level is open when all its channels are < n_open[e]);
+ * entries of closed levels are not touched. Summing calls over the symmetries of a sweep with
+ * g_s = the symmetry's statistical weight gives Omega_ab(E) = sum_s g_s sum |T^s_ij|^2 (DESIGN.md
+ * reading L1; the paper prints no formula). |T|^2 is formed as in rmx_collision_strength and
+ * never stored.
+ *   K            DEVICE [ne][nch][nch]
+ *   n_open       DEVICE int32 [ne] or NULL (= all open)
+ *   level_start  DEVICE int32 [nlevel + 1]: level a = channels [level_start[a], level_start[a+1]),
+ *                0 = level_start[0] < level_start[1] < ... <= nch (channels sorted by threshold,
+ *                the channels of a level contiguous; not checked on the host)
+ *   omega        DEVICE [ne][nlevel][nlevel], caller-initialised (accumulated into)
+ *   status       DEVICE int32 [ne] or NULL
+ * Per (e, a, b) the sum runs i ascending then j ascending: deterministic, no atomics.
+ * Errors: EINVAL on null K / level_start / omega, nlevel < 1, bad sizes.
+ */
+rmx_rc rmx_collision_strength_levels(rmx_ctx *ctx, const double *K, int64_t nch, int64_t ne,
+                                     const int32_t *n_open, const int32_t *level_start,
+                                     int64_t nlevel, double g, double *omega, int32_t *status);
+
+/*
  * rmx_sweep - the fused streaming driver: for energies in batches of `batch`, runs
  * build_R -> match_K -> collision_strength on ctx workspace (R and K never leave the
  * device), writing only the per-energy summaries rowsum [ne][nch] and status [ne].
@@ -137,6 +163,20 @@ rmx_rc rmx_sweep(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek, i
                  double *K_d, double *T2_d, double *rowsum, int32_t *status);
 
 /*
+ * rmx_sweep_levels - rmx_sweep whose T epilogue also accumulates the level-pair collision
+ * strengths of rmx_collision_strength_levels (omega [ne][nlevel][nlevel] += g * ...), fused:
+ * |T|^2 never leaves the chip. One call per symmetry (partial wave) of a multi-symmetry sweep,
+ * each with its own w, Ek, channels, F, G, F', G', n_open and level_start, the same E and omega.
+ * rowsum [ne][nch] may be NULL. Same argument rules as rmx_sweep (no dump list).
+ */
+rmx_rc rmx_sweep_levels(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek,
+                        int64_t nch, int64_t nlev, double a, const double *E, int64_t ne,
+                        const double *F, const double *G, const double *Fp, const double *Gp,
+                        const int32_t *n_open, int64_t batch, const int32_t *level_start,
+                        int64_t nlevel, double g, double *omega, double *rowsum,
+                        int32_t *status);
+
+/*
  * rmx_sweep_host - rmx_sweep with HOST inputs and outputs: copies w (as [nch][ldw]), Ek,
  * E, F, G, Fp, Gp, n_open host->device (staged through ctx pinned buffers), runs the sweep
  * and copies rowsum and status back, then synchronises the stream. status is fully
@@ -148,6 +188,47 @@ rmx_rc rmx_sweep_host(rmx_ctx *ctx, const double *w, int64_t ldw, const double *
                       const double *F, const double *G, const double *Fp, const double *Gp,
                       const int32_t *n_open, int64_t batch, double *rowsum, int32_t *status,
                       int64_t *h2d_bytes, int64_t *d2h_bytes);
+
+/* ---- NEXT-4 of SURVEY.md §8(f): post-processing on the energy mesh ------------------------ */
+
+/* largest number of temperatures per rmx_maxwell_average call */
+#define RMX_MAX_TEMPS 32
+
+/*
+ * rmx_convolve_gaussian - Gaussian convolution at a given FWHM with optional statistical
+ * admixture (Fig. 1 caption "convoluted with a 60 meV FWHM Gaussian";
+ * PAPER.md:370-373 Fig. 3 caption "appropriate Gaussian of FWHM and a statistical admixture of
+ * 2/3 ground and 1/3 metastable states"; operational definition, C1):
+ *     xbar = sum_m mix_m x_m / sum_m mix_m                  (mix == NULL: each spectrum alone)
+ *     y_i  = sum_{|j-i|<=M, 0<=j<ne} g_{j-i} xbar_j / sum_{same j} g_{j-i}
+ *     g_d  = exp(-(d dE)^2 / (2 s^2)), s = fwhm / (2 sqrt(2 ln 2)), M = floor(5 s / dE)
+ * on a UNIFORM mesh of spacing dE (kernel truncated at +-5 s, renormalised at the mesh edges).
+ *   x    DEVICE [nspec][ne]    spectra on the mesh (e.g. Omega_ab(E) or a row sum)
+ *   mix  HOST [nspec] or NULL  admixture weights (>= 0, any scale: 2:1 == 2/3, 1/3)
+ *   y    DEVICE [ne] if mix, else [nspec][ne]
+ * Errors: EINVAL on null x/y, dE or fwhm <= 0, fwhm < 2 dE (SPEC.md:299 UnderResolvedKernel),
+ * M > 9000, a negative weight or weights summing to 0. Async on the ctx stream (a call with mix
+ * synchronises the stream before returning, since mix is read from the caller's host buffer).
+ */
+rmx_rc rmx_convolve_gaussian(rmx_ctx *ctx, const double *x, int64_t nspec, const double *mix,
+                             int64_t ne, double dE, double fwhm, double *y);
+
+/*
+ * rmx_maxwell_average - Maxwellian-averaged (effective) collision strengths (SURVEY.md §8(f)
+ * item 4; reading U1; the paper prints no formula):
+ *     Ups_p(T) = int Omega_p(eps) exp(-eps/kT) d(eps/kT),  eps = E - Eth_p,
+ * by the trapezoid rule over the mesh points with E_i > Eth_p (no extrapolation).
+ *   omega  DEVICE [ne][npair]   Omega_p(E_i), row-major (pair fastest)
+ *   E      DEVICE [ne]          ascending mesh (need not be uniform)
+ *   Eth    DEVICE [npair]       excitation threshold of each pair (energy of the upper level)
+ *   kT     HOST [nT]            temperatures (energy units of E), 1 <= nT <= RMX_MAX_TEMPS
+ *   ups    DEVICE [npair][nT]   output
+ * Deterministic (fixed-order chunked sums, no atomics). Errors: EINVAL on null pointers, sizes < 1,
+ * nT out of range or kT <= 0.
+ */
+rmx_rc rmx_maxwell_average(rmx_ctx *ctx, const double *omega, int64_t ne, int64_t npair,
+                           const double *E, const double *Eth, const double *kT, int64_t nT,
+                           double *ups);
 
 /* Synchronise ctx's stream; if n_bad_status/status given, counts nonzero entries of the
  * DEVICE int32 status[ne] (pass status=NULL to skip). Returns sticky CUDA errors. */

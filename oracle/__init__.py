@@ -137,3 +137,69 @@ def sweep(w, Ek, a, E, F, G, Fp, Gp, n_open, idx, want=("R", "K", "T2", "rowsum"
                          _p(res["T2"]), _p(res["rowsum"]), _p(res["status"]),
                          _p(res["diag"]), int(threads or default_threads()))
     return {k: v for k, v in res.items() if v is not None}
+
+
+def level_omega(T2_, level_start, n_open: int, g: float = 1.0):
+    """Level-pair collision strengths of one symmetry (SURVEY.md §8(f) item 2; PAPER.md:143-146;
+    DESIGN.md reading L1): Omega_ab = g * sum_{i in a} sum_{j in b} |T_ij|^2 for the open levels
+    (all channels of the level < n_open), 0 for pairs involving a closed level. Plain loops over
+    the definition with long-double accumulation; T2_ is the oracle's |T|^2 [nch, nch]."""
+    ls = [int(x) for x in level_start]
+    nlevel = len(ls) - 1
+    om = np.zeros((nlevel, nlevel))
+    T2l = np.asarray(T2_, dtype=np.longdouble)
+    for la in range(nlevel):
+        if ls[la + 1] > n_open:
+            continue
+        for lb in range(nlevel):
+            if ls[lb + 1] > n_open:
+                continue
+            acc = T2l[ls[la]:ls[la + 1], ls[lb]:ls[lb + 1]].sum()  # the block's entries
+            om[la, lb] = float(np.longdouble(g) * acc)
+    return om
+
+
+def convolve_gaussian(x, dE: float, fwhm: float, mix=None):
+    """Gaussian convolution with statistical admixture (PAPER.md:298-300, 370-373 figure captions;
+    operational definition; reading C1), written out per output point:
+    s = fwhm/(2 sqrt(2 ln 2)), M = floor(5 s/dE), y_i = sum_j g(E_j - E_i) xbar_j / sum_j g(E_j - E_i)
+    over 0 <= j < ne with |j - i| <= M, g(u) = exp(-u^2/(2 s^2)), xbar = sum_m c_m x_m / sum_m c_m.
+    Long-double accumulation, j ascending. x: [nspec, ne] or [ne]."""
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    nspec, ne = x.shape
+    if mix is not None:
+        c = np.asarray(mix, dtype=np.longdouble)
+        xs = [(c[:, None] * x.astype(np.longdouble)).sum(axis=0) / c.sum()]
+    else:
+        xs = [x[m].astype(np.longdouble) for m in range(nspec)]
+    s = fwhm / (2.0 * np.sqrt(2.0 * np.log(2.0)))
+    M = int(np.floor(5.0 * s / dE))
+    d = np.arange(-M, M + 1)
+    g = np.exp(-((d * dE) ** 2) / (2.0 * s * s)).astype(np.longdouble)
+    out = np.empty((len(xs), ne))
+    for m, xb in enumerate(xs):
+        for i in range(ne):
+            lo, hi = max(0, i - M), min(ne - 1, i + M)
+            gw = g[lo - i + M:hi - i + M + 1]
+            out[m, i] = float((gw * xb[lo:hi + 1]).sum() / gw.sum())
+    return out[0] if mix is not None else out
+
+
+def maxwell_average(omega, E, Eth, kT):
+    """Maxwellian average Ups_p(T) = int Omega_p(eps) e^{-eps/kT} d(eps/kT), eps = E - Eth_p
+    (reading U1), by the trapezoid rule over the mesh points with
+    E_i > Eth_p: sum over intervals (E_{i+1} - E_i)(f_i + f_{i+1})/2, f = Omega e^{-eps/kT}/kT.
+    omega: [ne, npair]; returns [npair, nT]."""
+    omega = np.asarray(omega, dtype=np.float64)
+    E = np.asarray(E, dtype=np.longdouble)
+    ne, npair = omega.shape
+    out = np.zeros((npair, len(kT)))
+    for p in range(npair):
+        first = int(np.searchsorted(np.asarray(E, dtype=np.float64), Eth[p], side="right"))
+        for t, kt in enumerate(kT):
+            kt = np.longdouble(kt)
+            f = omega[first:, p].astype(np.longdouble) * np.exp(-(E[first:] - np.longdouble(Eth[p])) / kt) / kt
+            Ei = E[first:]
+            acc = ((Ei[1:] - Ei[:-1]) * (f[:-1] + f[1:]) / 2).sum()  # the trapezoids, summed
+            out[p, t] = float(acc)
+    return out

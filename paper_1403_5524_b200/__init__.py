@@ -31,7 +31,9 @@ KID_NAMES = ("rform", "match", "tepi", "other")
 
 # every symbol include/rmx.h declares (tests/test_abi.py checks the header and the .so agree)
 EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rmx_build_R",
-            "rmx_match_K", "rmx_collision_strength", "rmx_sweep", "rmx_sweep_host", "rmx_sync",
+            "rmx_match_K", "rmx_collision_strength", "rmx_collision_strength_levels", "rmx_sweep",
+            "rmx_sweep_levels", "rmx_sweep_host", "rmx_convolve_gaussian", "rmx_maxwell_average",
+            "rmx_sync",
             "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version", "rmx_sm_target")
 
 
@@ -59,8 +61,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "rmx_build_R": [P, P, i64, P, i64, i64, d, P, i64, P, P],
         "rmx_match_K": [P, P, P, P, P, P, d, i64, i64, P, P, P],
         "rmx_collision_strength": [P, P, i64, i64, P, P, P, P],
+        "rmx_collision_strength_levels": [P, P, i64, i64, P, P, i64, d, P, P],
         "rmx_sweep": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, i64, P, P, P, P, P],
+        "rmx_sweep_levels": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, i64, d, P, P,
+                             P],
         "rmx_sweep_host": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, P, P, P],
+        "rmx_convolve_gaussian": [P, P, i64, P, i64, d, d, P],
+        "rmx_maxwell_average": [P, P, i64, i64, P, P, P, i64, P],
         "rmx_sync": [P, P, i64, P],
         "rmx_set_timing": [P, i32],
         "rmx_reset_stats": [P],
@@ -198,7 +205,51 @@ class Context:
                     "rmx_collision_strength")
         return T2, rs, status
 
+    def collision_strength_levels(self, K, level_start, g: float = 1.0, n_open=None, omega=None,
+                                  status=None):
+        """rmx_collision_strength_levels: omega[e][a][b] += g sum_{i in a, j in b} |T_ij|^2 over
+        the open levels. Returns (omega [ne,nlevel,nlevel], status)."""
+        torch = _torch()
+        self._bind_stream()
+        K = self._dev(K, torch.float64)
+        ne, nch = K.shape[0], K.shape[1]
+        ls = self._dev(level_start, torch.int32)
+        nlevel = ls.numel() - 1
+        no = None if n_open is None else self._dev(n_open, torch.int32)
+        if omega is None:
+            omega = torch.zeros((ne, nlevel, nlevel), dtype=torch.float64, device=K.device)
+        status = self._status(status, ne)
+        self._check(self.lib.rmx_collision_strength_levels(
+            self._h, _ptr(K), nch, ne, _ptr(no), _ptr(ls), nlevel, float(g), _ptr(omega),
+            _ptr(status)), "rmx_collision_strength_levels")
+        return omega, status
+
     # ------------------------------------------------------------------ fused drivers
+    def sweep_levels(self, w, Ek, a: float, E, F, G, Fp, Gp, n_open, level_start, g: float = 1.0,
+                     omega=None, rowsum=None, batch: int = 0, status=None, want_rowsum=False):
+        """rmx_sweep_levels: the fused sweep of one symmetry accumulating
+        omega[e][a][b] += g sum_{i in a, j in b} |T_ij(E_e)|^2. Returns dict(omega, rowsum, status)."""
+        torch = _torch()
+        self._bind_stream()
+        w, nlev, ldw = self.prepare_w(w)
+        Ek = self._dev(Ek, torch.float64)
+        E = self._dev(E, torch.float64)
+        F, G, Fp, Gp = (self._dev(x, torch.float64) for x in (F, G, Fp, Gp))
+        n_open = None if n_open is None else self._dev(n_open, torch.int32)
+        ls = self._dev(level_start, torch.int32)
+        nlevel = ls.numel() - 1
+        nch, ne = w.shape[0], E.shape[0]
+        if omega is None:
+            omega = torch.zeros((ne, nlevel, nlevel), dtype=torch.float64, device=w.device)
+        if rowsum is None and want_rowsum:
+            rowsum = torch.empty((ne, nch), dtype=torch.float64, device=w.device)
+        status = self._status(status, ne)
+        self._check(self.lib.rmx_sweep_levels(
+            self._h, _ptr(w), ldw, _ptr(Ek), nch, nlev, float(a), _ptr(E), ne, _ptr(F), _ptr(G),
+            _ptr(Fp), _ptr(Gp), _ptr(n_open), int(batch), _ptr(ls), nlevel, float(g), _ptr(omega),
+            _ptr(rowsum), _ptr(status)), "rmx_sweep_levels")
+        return {"omega": omega, "rowsum": rowsum, "status": status}
+
     def sweep(self, w, Ek, a: float, E, F, G, Fp, Gp, n_open=None, batch: int = 0,
               dump_idx: Optional[Sequence[int]] = None, status=None, rowsum=None, prepared=False):
         """rmx_sweep: R -> K -> |T|^2 for all energies; returns dict with rowsum [ne,nch], status
@@ -255,6 +306,38 @@ class Context:
             P(n_open), int(batch), P(rowsum), P(status), ctypes.byref(h2d), ctypes.byref(d2h)),
             "rmx_sweep_host")
         return rowsum, status, h2d.value, d2h.value
+
+    # ------------------------------------------------------------------ post-processing
+    def convolve_gaussian(self, x, dE: float, fwhm: float, mix=None):
+        """rmx_convolve_gaussian: x [nspec, ne] (or [ne]) on a uniform mesh of spacing dE ->
+        Gaussian-convolved spectra ([nspec, ne]) or, with admixture weights mix [nspec], one [ne]."""
+        torch = _torch()
+        self._bind_stream()
+        x = self._dev(x, torch.float64)
+        if x.dim() == 1:
+            x = x[None, :]
+        nspec, ne = x.shape
+        mixh = None if mix is None else np.ascontiguousarray(mix, dtype=np.float64)
+        y = torch.empty((ne,) if mixh is not None else (nspec, ne), dtype=torch.float64, device=x.device)
+        self._check(self.lib.rmx_convolve_gaussian(
+            self._h, _ptr(x), nspec, None if mixh is None else mixh.ctypes.data_as(ctypes.c_void_p),
+            ne, float(dE), float(fwhm), _ptr(y)), "rmx_convolve_gaussian")
+        return y
+
+    def maxwell_average(self, omega, E, Eth, kT):
+        """rmx_maxwell_average: omega [ne, npair] -> Upsilon [npair, nT]."""
+        torch = _torch()
+        self._bind_stream()
+        omega = self._dev(omega, torch.float64)
+        E = self._dev(E, torch.float64)
+        Eth = self._dev(Eth, torch.float64)
+        kTh = np.ascontiguousarray(kT, dtype=np.float64)
+        ne, npair = omega.shape
+        ups = torch.empty((npair, len(kTh)), dtype=torch.float64, device=omega.device)
+        self._check(self.lib.rmx_maxwell_average(self._h, _ptr(omega), ne, npair, _ptr(E), _ptr(Eth),
+                                                 kTh.ctypes.data_as(ctypes.c_void_p), len(kTh),
+                                                 _ptr(ups)), "rmx_maxwell_average")
+        return ups
 
     # ------------------------------------------------------------------ instrumentation
     def set_timing(self, on: bool = True):
@@ -315,3 +398,21 @@ def rmx_collision_strength(K, n_open=None, status=None):
 
 def rmx_sweep(w, Ek, a, E, F, G, Fp, Gp, n_open=None, batch=0, dump_idx=None):
     return _ctx().sweep(w, Ek, a, E, F, G, Fp, Gp, n_open=n_open, batch=batch, dump_idx=dump_idx)
+
+
+def rmx_collision_strength_levels(K, level_start, g=1.0, n_open=None, omega=None, status=None):
+    return _ctx().collision_strength_levels(K, level_start, g=g, n_open=n_open, omega=omega,
+                                            status=status)
+
+
+def rmx_convolve_gaussian(x, dE, fwhm, mix=None):
+    return _ctx().convolve_gaussian(x, dE, fwhm, mix=mix)
+
+
+def rmx_maxwell_average(omega, E, Eth, kT):
+    return _ctx().maxwell_average(omega, E, Eth, kT)
+
+
+def rmx_sweep_levels(w, Ek, a, E, F, G, Fp, Gp, n_open, level_start, g=1.0, omega=None, batch=0):
+    return _ctx().sweep_levels(w, Ek, a, E, F, G, Fp, Gp, n_open, level_start, g=g, omega=omega,
+                               batch=batch)

@@ -37,6 +37,8 @@ struct rmx_ctx {
     void *p = nullptr;
     size_t bytes = 0;
   } dw, dEk, dE, dF, dG, dFp, dGp, dno, drs, dst;
+  // post-processing scratch (NEXT-4): Gaussian weight table, admixture weights, Maxwell partials
+  Dev dgt, dmix, dpart;
   // instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> free_events;
@@ -190,7 +192,7 @@ rmx_rc check_sticky(rmx_ctx *c) {
 
 extern "C" {
 
-int rmx_version(void) { return 100; }
+int rmx_version(void) { return 200; }
 int rmx_sm_target(void) { return 100; }
 
 rmx_rc rmx_create(rmx_ctx **ctx, int device, void *stream) {
@@ -293,10 +295,46 @@ rmx_rc rmx_collision_strength(rmx_ctx *c, const double *K, int64_t nch, int64_t 
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
-    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, c->ws, ws_slot_doubles(nch), c->tepi_views,
-                       slots, status, c->stream);
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, LevelSums{}, c->ws,
+                       ws_slot_doubles(nch), c->tepi_views, slots, status, c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_collision_strength");
+  return RMX_OK;
+}
+
+// host-side validation of a level partition: 0 = level_start[0] < ... <= nch (the array itself is
+// on the device; only nlevel and the pointer can be checked synchronously)
+static rmx_rc check_levels(rmx_ctx *c, const char *who, const int32_t *level_start, int64_t nlevel,
+                           const double *omega) {
+  if (!level_start || !omega) return fail(c, RMX_EINVAL, std::string(who) + ": null level_start / omega");
+  if (nlevel < 1 || nlevel > (1 << 16)) return fail(c, RMX_EINVAL, std::string(who) + ": bad nlevel");
+  return RMX_OK;
+}
+
+rmx_rc rmx_collision_strength_levels(rmx_ctx *c, const double *K, int64_t nch, int64_t ne,
+                                     const int32_t *n_open, const int32_t *level_start,
+                                     int64_t nlevel, double g, double *omega, int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!K) return fail(c, RMX_EINVAL, "rmx_collision_strength_levels: null K");
+  if (nch < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_collision_strength_levels: sizes must be >= 1");
+  if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_collision_strength_levels: nch too large");
+  rmx_rc rc = check_levels(c, "rmx_collision_strength_levels", level_start, nlevel, omega);
+  if (rc != RMX_OK) return rc;
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  const int64_t slots = ws_slots_for(c, ne);
+  rc = ensure_ws(c, nch, slots);
+  if (rc != RMX_OK) return rc;
+  LevelSums lv;
+  lv.level_start = level_start;
+  lv.nlevel = static_cast<int>(nlevel);
+  lv.g = g;
+  lv.omega = omega;
+  cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, nullptr, nullptr, nullptr, lv, c->ws,
+                       ws_slot_doubles(nch), c->tepi_views, slots, status, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_collision_strength_levels");
   return RMX_OK;
 }
 
@@ -308,13 +346,14 @@ static int64_t default_batch(const rmx_ctx *c, int64_t nch, int64_t ne) {
   return std::min<int64_t>(b, ne);
 }
 
-rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
-                 int64_t nlev, double a, const double *E, int64_t ne, const double *F,
-                 const double *G, const double *Fp, const double *Gp, const int32_t *n_open,
-                 int64_t batch, const int64_t *dump_idx, int64_t n_dump, double *R_d,
-                 double *K_d, double *T2_d, double *rowsum, int32_t *status) {
+static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                         int64_t nlev, double a, const double *E, int64_t ne, const double *F,
+                         const double *G, const double *Fp, const double *Gp,
+                         const int32_t *n_open, int64_t batch, const int64_t *dump_idx,
+                         int64_t n_dump, double *R_d, double *K_d, double *T2_d, double *rowsum,
+                         const LevelSums &lv, int32_t *status) {
   if (!c) return RMX_EINVAL;
-  if (!w || !Ek || !E || !F || !G || !Fp || !Gp || !rowsum)
+  if (!w || !Ek || !E || !F || !G || !Fp || !Gp || (!rowsum && !lv.omega))
     return fail(c, RMX_EINVAL, "rmx_sweep: null pointer");
   if (nch < 1 || nlev < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_sweep: sizes must be >= 1");
   if (nch > kMaxMatchChannels)
@@ -365,18 +404,49 @@ rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int
       if (T2_d) {
         e = timed(c, RMX_KID_TEPI, 1, [&] {
           return launch_tepi(rb + l * mat, nch, mat, nch, 1, nob ? nob + l : nullptr, T2_d + d * mat,
-                             nullptr, nullptr, c->ws, ws_slot_doubles(nch), c->tepi_views, 1, nullptr, c->stream);
+                             nullptr, nullptr, LevelSums{}, c->ws, ws_slot_doubles(nch), c->tepi_views, 1, nullptr, c->stream);
         });
         if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T dump");
       }
     }
+    LevelSums lvb = lv;
+    if (lvb.omega) lvb.omega += b0 * static_cast<int64_t>(lv.nlevel) * lv.nlevel;
     e = timed(c, RMX_KID_TEPI, 1, [&] {
-      return launch_tepi(rb, nch, mat, nch, nb, nob, nullptr, nullptr, rowsum + b0 * nch, c->ws,
-                         ws_slot_doubles(nch), c->tepi_views, slots, stb, c->stream);
+      return launch_tepi(rb, nch, mat, nch, nb, nob, nullptr, nullptr,
+                         rowsum ? rowsum + b0 * nch : nullptr, lvb, c->ws, ws_slot_doubles(nch),
+                         c->tepi_views, slots, stb, c->stream);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T");
   }
   return RMX_OK;
+}
+
+rmx_rc rmx_sweep(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                 int64_t nlev, double a, const double *E, int64_t ne, const double *F,
+                 const double *G, const double *Fp, const double *Gp, const int32_t *n_open,
+                 int64_t batch, const int64_t *dump_idx, int64_t n_dump, double *R_d,
+                 double *K_d, double *T2_d, double *rowsum, int32_t *status) {
+  if (c && !rowsum) return fail(c, RMX_EINVAL, "rmx_sweep: null rowsum");
+  return sweep_impl(c, w, ldw, Ek, nch, nlev, a, E, ne, F, G, Fp, Gp, n_open, batch, dump_idx,
+                    n_dump, R_d, K_d, T2_d, rowsum, LevelSums{}, status);
+}
+
+rmx_rc rmx_sweep_levels(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                        int64_t nlev, double a, const double *E, int64_t ne, const double *F,
+                        const double *G, const double *Fp, const double *Gp,
+                        const int32_t *n_open, int64_t batch, const int32_t *level_start,
+                        int64_t nlevel, double g, double *omega, double *rowsum,
+                        int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  rmx_rc rc = check_levels(c, "rmx_sweep_levels", level_start, nlevel, omega);
+  if (rc != RMX_OK) return rc;
+  LevelSums lv;
+  lv.level_start = level_start;
+  lv.nlevel = static_cast<int>(nlevel);
+  lv.g = g;
+  lv.omega = omega;
+  return sweep_impl(c, w, ldw, Ek, nch, nlev, a, E, ne, F, G, Fp, Gp, n_open, batch, nullptr, 0,
+                    nullptr, nullptr, nullptr, rowsum, lv, status);
 }
 
 rmx_rc rmx_sweep_host(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
@@ -427,6 +497,63 @@ rmx_rc rmx_sweep_host(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep_host/d2h");
   if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(bw + bek + be + 4 * bf + (n_open ? bno : 0));
   if (d2h_bytes) *d2h_bytes = static_cast<int64_t>(bf + bno);
+  return RMX_OK;
+}
+
+rmx_rc rmx_convolve_gaussian(rmx_ctx *c, const double *x, int64_t nspec, const double *mix,
+                             int64_t ne, double dE, double fwhm, double *y) {
+  if (!c) return RMX_EINVAL;
+  if (!x || !y) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: null pointer");
+  if (nspec < 1 || ne < 1 || nspec > 4096) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: bad sizes");
+  if (!(dE > 0.0) || !(fwhm > 0.0)) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: dE, fwhm must be > 0");
+  if (fwhm < 2.0 * dE) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: fwhm < 2 dE (under-resolved kernel)");
+  const int M = conv_window(dE, fwhm, nullptr);
+  if (M > kMaxConvHalfWidth)
+    return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: window 5 sigma / dE > " + std::to_string(kMaxConvHalfWidth));
+  double msum = 0.0;
+  if (mix)
+    for (int64_t m = 0; m < nspec; ++m) {
+      if (!(mix[m] >= 0.0)) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: negative admixture weight");
+      msum += mix[m];
+    }
+  if (mix && !(msum > 0.0)) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: admixture weights sum to 0");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  rmx_rc rc;
+  if ((rc = grow(c, c->dgt, sizeof(double) * (M + 1))) ||
+      (mix && (rc = grow(c, c->dmix, sizeof(double) * nspec))))
+    return rc;
+  cudaError_t e = cudaSuccess;
+  if (mix) e = cudaMemcpyAsync(c->dmix.p, mix, sizeof(double) * nspec, cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_convolve_gaussian/mix");
+  e = timed(c, RMX_KID_OTHER, 2, [&] {
+    return launch_convolve(x, nspec, mix ? static_cast<double *>(c->dmix.p) : nullptr, ne, dE, fwhm,
+                           static_cast<double *>(c->dgt.p), y, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_convolve_gaussian");
+  if (mix) cudaStreamSynchronize(c->stream);  // mix is a caller host buffer copied asynchronously
+  return RMX_OK;
+}
+
+rmx_rc rmx_maxwell_average(rmx_ctx *c, const double *omega, int64_t ne, int64_t npair,
+                           const double *E, const double *Eth, const double *kT, int64_t nT,
+                           double *ups) {
+  if (!c) return RMX_EINVAL;
+  if (!omega || !E || !Eth || !kT || !ups) return fail(c, RMX_EINVAL, "rmx_maxwell_average: null pointer");
+  if (ne < 1 || npair < 1) return fail(c, RMX_EINVAL, "rmx_maxwell_average: sizes must be >= 1");
+  if (nT < 1 || nT > RMX_MAX_TEMPS)
+    return fail(c, RMX_EINVAL, "rmx_maxwell_average: 1 <= nT <= RMX_MAX_TEMPS");
+  for (int64_t t = 0; t < nT; ++t)
+    if (!(kT[t] > 0.0)) return fail(c, RMX_EINVAL, "rmx_maxwell_average: kT must be > 0");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  rmx_rc rc = grow(c, c->dpart, sizeof(double) * maxwell_chunks(ne) * npair * nT);
+  if (rc != RMX_OK) return rc;
+  cudaError_t e = timed(c, RMX_KID_OTHER, 2, [&] {
+    return launch_maxwell(omega, ne, npair, E, Eth, kT, static_cast<int>(nT),
+                          static_cast<double *>(c->dpart.p), ups, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_maxwell_average");
   return RMX_OK;
 }
 

@@ -62,12 +62,31 @@ cudaError_t launch_match(const double *R, const double *F, const double *G, cons
                          int32_t *status, cudaStream_t st);
 
 // tepi.cu
+// Optional level-pair output of the T epilogue (NEXT-2): omega [ne][nlevel][nlevel] accumulates
+// g * sum_{i in a, j in b} |T_ij|^2 over the open levels; level a = channels
+// [level_start[a], level_start[a+1]) (DEVICE int32 [nlevel + 1]). omega == nullptr: off.
+struct LevelSums {
+  const int32_t *level_start = nullptr;
+  int nlevel = 0;
+  double g = 0.0;
+  double *omega = nullptr;
+};
 int64_t tepi_ws_doubles_per_slot(int64_t nch);
 void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs);
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
-                        double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
-                        int32_t *status, cudaStream_t st);
+                        const LevelSums &lv, double *ws, int64_t ws_slot, const CUtensorMap *views,
+                        int64_t ws_slots, int32_t *status, cudaStream_t st);
+
+// post.cu (NEXT-4); the Gaussian window x[i-M, i+256+M) and its weights live in shared memory
+constexpr int kMaxConvHalfWidth = 9000;
+int conv_window(double dE, double fwhm, double *sigma);
+cudaError_t launch_convolve(const double *x, int64_t nspec, const double *mix_dev, int64_t ne,
+                            double dE, double fwhm, double *gtab, double *y, cudaStream_t st);
+int64_t maxwell_chunks(int64_t ne);
+cudaError_t launch_maxwell(const double *omega, int64_t ne, int64_t npair, const double *E,
+                           const double *Eth, const double *kT, int nT, double *part, double *ups,
+                           cudaStream_t st);
 
 // largest channel count the matching kernel supports: its LU sub-panels (n x 9 doubles) are
 // staged in the ~216 KB shared-memory union of the kernel

@@ -58,8 +58,8 @@ __device__ __forceinline__ void mirror_lower(double *P, int64_t ld, int o, doubl
 __global__ void __launch_bounds__(NT, 1)
     tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
                 const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
-                double *rowsum, double *ws, int64_t ws_slot, const CUtensorMap *views,
-                int32_t *status) {
+                double *rowsum, LevelSums lv, double *ws, int64_t ws_slot,
+                const CUtensorMap *views, int32_t *status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TepiSmem &sm = *reinterpret_cast<TepiSmem *>(smem_raw);
   const TepiLayout L = tepi_layout(n);
@@ -170,6 +170,27 @@ __global__ void __launch_bounds__(NT, 1)
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (rowsum && lane_id() == 0) rowsum[e * n + i] = s;
     }
+    if (lv.omega && o > 0) {
+      // NEXT-2: level-pair collision strengths
+      //   Omega_ab += g sum_{i in a} sum_{j in b} |T_ij|^2
+      // for the open levels (channel ranges [ls[a], ls[a+1]) inside [0, o)). One warp per level
+      // a, one lane per level b; i ascending, then j ascending (fixed order, no atomics).
+      int nlo = 0;
+      while (nlo < lv.nlevel && lv.level_start[nlo + 1] <= o) ++nlo;
+      double *Om = lv.omega + e * lv.nlevel * lv.nlevel;
+      for (int la = warp_id(); la < nlo; la += NW) {
+        const int i0 = lv.level_start[la], i1 = lv.level_start[la + 1];
+        for (int lb = lane_id(); lb < nlo; lb += 32) {
+          const int j0 = lv.level_start[lb], j1 = lv.level_start[lb + 1];
+          double acc = 0.0;
+          for (int i = i0; i < i1; ++i) {
+            const double *xr = Xv.at(i, 0), *pr = Sv.at(i, 0);
+            for (int j = j0; j < j1; ++j) acc += 4.0 * fma(xr[j], xr[j], pr[j] * pr[j]);
+          }
+          Om[static_cast<int64_t>(la) * lv.nlevel + lb] += lv.g * acc;
+        }
+      }
+    }
     bad = __syncthreads_or(bad);
     if (bad && threadIdx.x == 0) set_status(status, e, RMX_E_NONFINITE);
   }
@@ -186,8 +207,8 @@ void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
-                        double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
-                        int32_t *status, cudaStream_t st) {
+                        const LevelSums &lv, double *ws, int64_t ws_slot, const CUtensorMap *views,
+                        int64_t ws_slots, int32_t *status, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t ce = cudaFuncSetAttribute(tepi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -197,7 +218,7 @@ cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t n
   }
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
   tepi_kernel<<<grid, NT, sizeof(TepiSmem), st>>>(K, ldk, kstride, static_cast<int>(nch), ne, n_open,
-                                                  T2, t2_slot, rowsum, ws, ws_slot, views, status);
+                                                  T2, t2_slot, rowsum, lv, ws, ws_slot, views, status);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ import numpy as np
 
 __all__ = [
     "Case", "CONFIGS", "make_case", "asymptotic", "n_open", "mesh", "brute_force_case",
-    "parity_sample",
+    "parity_sample", "level_start", "symmetry_cases",
 ]
 
 
@@ -246,3 +246,39 @@ def parity_sample(case: Case, n_even: int, n_pole: int = 4, n_thresh: int = 4) -
             if 0 <= j < ne:
                 idx.add(j)
     return np.array(sorted(idx), dtype=np.int64)
+
+
+def level_start(eps: np.ndarray) -> np.ndarray:
+    """Level partition of the (threshold-sorted) channels: channels sharing one threshold belong to
+    one target level (BASELINE.json:10 'each level spawning ~6-7 channels'). Returns int32
+    [nlevel + 1] with level a = channels [ls[a], ls[a+1]). Pure input structure, no arithmetic of
+    the method."""
+    eps = np.asarray(eps, dtype=np.float64)
+    cut = np.flatnonzero(np.diff(eps) != 0.0) + 1
+    return np.concatenate([[0], cut, [len(eps)]]).astype(np.int32)
+
+
+def symmetry_cases(nsym: int, nlevel: int, seed: int, nlev: int = 300, ne: int = 8,
+                   lo: float = 0.5, hi: float = 6.0, a: float = 12.0, lev_hi: float = 4.0,
+                   max_ch: int = 3):
+    """Several symmetries (partial waves) over ONE set of target levels, for the level-pair
+    collision strengths of SURVEY.md §8(f) item 2: the level energies
+    (thresholds) ~ U[0, lev_hi] are shared; symmetry s couples level a through c_sa ~ U{1..max_ch}
+    channels, has its own poles E_k ~ U[-1, 40] (sorted) and amplitudes w ~ N(0, 0.3^2). All
+    symmetries share the energy mesh. Returns (levels [nlevel], E [ne], [(Case, level_start), ...])."""
+    rng = np.random.default_rng(seed)
+    lev = np.sort(rng.uniform(0.0, lev_hi, nlevel))
+    E = mesh(lo, hi, ne)
+    out = []
+    for s in range(nsym):
+        cnt = rng.integers(1, max_ch + 1, nlevel)
+        eps = np.repeat(lev, cnt)
+        nch = len(eps)
+        Ek = np.sort(rng.uniform(-1.0, 40.0, nlev))
+        w = rng.normal(0.0, 0.3, (nch, nlev))
+        Es, _ = _drop_near_poles(E, Ek, 1e-6)
+        assert len(Es) == len(E), "mesh point within 1e-6 of a pole: pick another seed"
+        case = Case(name=f"sym{s}", w=np.ascontiguousarray(w), Ek=Ek, eps=eps, E=E.copy(), a=a)
+        ls = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32)
+        out.append((case, ls))
+    return lev, E, out

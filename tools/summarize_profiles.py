@@ -17,14 +17,14 @@ launches = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out"
 rep = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "prof_round.ncu-rep")
 out_dir = os.path.join(ROOT, "profiles")
 
-# ---- launch list -------------------------------------------------------------------------------
-rows = list(csv.reader(open(launches)))
-hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
-hdr = rows[hi]
+# ---- launch list ("-" skips it) ----------------------------------------------------------------
+rows = list(csv.reader(open(launches))) if launches != "-" else []
+hi = next((i for i, r in enumerate(rows) if r and r[0] == "ID"), None)
+hdr = rows[hi] if hi is not None else []
 col = {h: i for i, h in enumerate(hdr)}
 agg = collections.OrderedDict()
 scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
-for r in rows[hi + 1:]:
+for r in (rows[hi + 1:] if hi is not None else []):
     if len(r) != len(hdr) or r[col["Metric Name"]] != "gpu__time_duration.sum":
         continue
     name = r[col["Kernel Name"]].split("(")[0][:70]
@@ -32,9 +32,9 @@ for r in rows[hi + 1:]:
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
     a[1] += v
-tot = sum(v[1] for v in agg.values())
+tot = sum(v[1] for v in agg.values()) or 1.0
 ours = {k: v for k, v in agg.items() if any(s in k for s in ("rform", "match_kernel", "tepi_kernel"))}
-tot_ours = sum(v[1] for v in ours.values())
+tot_ours = sum(v[1] for v in ours.values()) or 1.0
 lines = [f"# Round {rnd} ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
          "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline` (darc, 296 energies/step).",
          "Per-launch times are cold-cache and serialised: compare shares, not absolutes.", "",
@@ -42,15 +42,17 @@ lines = [f"# Round {rnd} ncu launch list (gpu__time_duration.sum, --clock-contro
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:15]:
     lines.append(f"| `{k}` | {v[0]} | {v[1]:.1f} | {100 * v[1] / tot:.1f}% | "
                  f"{(100 * v[1] / tot_ours) if k in ours else 0:.1f}% |")
-open(os.path.join(out_dir, f"r{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
-print("\n".join(lines))
+if agg:
+    open(os.path.join(out_dir, f"r{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
 
 # ---- full capture ------------------------------------------------------------------------------
 metrics = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
            "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size",
            "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
-           "smsp__inst_executed.sum"]
+           "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
 if os.path.exists(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
@@ -74,6 +76,9 @@ if os.path.exists(rep):
                 ent[m.replace(".sum", ".bytes")] = ent[m] * f
         ent["workload"] = {"config": "darc", "energies_per_launch": 296}
         res.setdefault(name, ent)
-    json.dump(res, open(os.path.join(out_dir, f"r{rnd}_ncu_kernels.json"), "w"), indent=1)
+    path = os.path.join(out_dir, f"r{rnd}_ncu_kernels.json")
+    old = json.load(open(path)) if os.path.exists(path) else {}
+    old.update(res)  # kernels captured in this report replace their older entries
+    json.dump(old, open(path, "w"), indent=1)
     for k, v in res.items():
         print(k, {m: v[m] for m in metrics[:5]})
