@@ -189,6 +189,26 @@ rmx_rc rmx_sweep_host(rmx_ctx *ctx, const double *w, int64_t ldw, const double *
                       const int32_t *n_open, int64_t batch, double *rowsum, int32_t *status,
                       int64_t *h2d_bytes, int64_t *d2h_bytes);
 
+/* ---- NEXT-3 of SURVEY.md §8(f): the inner-region step that feeds the sweep ------------------ */
+
+/*
+ * rmx_inner_region - full dense eigensolve of the (synthetic) inner-region Hamiltonian and the
+ * boundary amplitudes of its eigenstates ("The diagonalization of each matrix,
+ * from which every eigenvalue and every eigenvector is required ... pdsyevd"; SURVEY.md §8(f)
+ * item 3): (E_k, V) = eigh(H) by cuSOLVER syevd (library, like the paper's ScaLAPACK pdsyevd),
+ * then w = P^T V by one cuBLAS DGEMM, where P [nlev][nch] are the channel projections of the basis
+ * at r = a. The outputs are exactly the (E_k, w) inputs of rmx_build_R / rmx_sweep:
+ * (1/2a) W diag(1/(E_k - E)) W^T = (1/2a) P^T (H - E)^{-1} P.
+ *   H    DEVICE [nlev][nlev]  symmetric (read only; the lower triangle is used)
+ *   P    DEVICE [nlev][nch]
+ *   Ek   DEVICE [nlev]        eigenvalues, ascending
+ *   w    DEVICE [nch][ldw]    amplitudes (ldw >= nlev; columns nlev..ldw-1 untouched)
+ * Eigenvector signs are those of the solver (R, K, T do not depend on them). Synchronous (waits
+ * for the solver's info). Errors: EINVAL on null pointers / bad sizes; ECUDA if the solver fails.
+ */
+rmx_rc rmx_inner_region(rmx_ctx *ctx, const double *H, int64_t nlev, const double *P, int64_t nch,
+                        double *Ek, double *w, int64_t ldw);
+
 /* ---- NEXT-4 of SURVEY.md §8(f): post-processing on the energy mesh ------------------------ */
 
 /* largest number of temperatures per rmx_maxwell_average call */

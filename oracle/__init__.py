@@ -203,3 +203,11 @@ def maxwell_average(omega, E, Eth, kT):
             acc = ((Ei[1:] - Ei[:-1]) * (f[:-1] + f[1:]) / 2).sum()  # the trapezoids, summed
             out[p, t] = float(acc)
     return out
+
+
+def inner_region(H, P):
+    """Inner-region step feeding the sweep ('every eigenvalue and every
+    eigenvector is required', ScaLAPACK pdsyevd): (E_k, V) = eigh(H)
+    (LAPACK via numpy - a library primitive used as the step), w = P^T V. Returns (Ek, w [nch, nlev])."""
+    Ek, V = np.linalg.eigh(np.asarray(H, dtype=np.float64))
+    return Ek, np.ascontiguousarray(np.asarray(P, dtype=np.float64).T @ V)

@@ -32,7 +32,8 @@ KID_NAMES = ("rform", "match", "tepi", "other")
 # every symbol include/rmx.h declares (tests/test_abi.py checks the header and the .so agree)
 EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rmx_build_R",
             "rmx_match_K", "rmx_collision_strength", "rmx_collision_strength_levels", "rmx_sweep",
-            "rmx_sweep_levels", "rmx_sweep_host", "rmx_convolve_gaussian", "rmx_maxwell_average",
+            "rmx_sweep_levels", "rmx_sweep_host", "rmx_inner_region", "rmx_convolve_gaussian",
+            "rmx_maxwell_average",
             "rmx_sync",
             "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version", "rmx_sm_target")
 
@@ -66,6 +67,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "rmx_sweep_levels": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, i64, d, P, P,
                              P],
         "rmx_sweep_host": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, P, P, P],
+        "rmx_inner_region": [P, P, i64, P, i64, P, P, i64],
         "rmx_convolve_gaussian": [P, P, i64, P, i64, d, d, P],
         "rmx_maxwell_average": [P, P, i64, i64, P, P, P, i64, P],
         "rmx_sync": [P, P, i64, P],
@@ -307,6 +309,22 @@ class Context:
             "rmx_sweep_host")
         return rowsum, status, h2d.value, d2h.value
 
+    # ------------------------------------------------------------------ inner region (NEXT-3)
+    def inner_region(self, H, P):
+        """rmx_inner_region: (E_k, V) = eigh(H), w = P^T V. Returns (Ek [nlev], w [nch, ldw], nlev,
+        ldw) with ldw even (ready for build_R / sweep with prepared=(nlev, ldw))."""
+        torch = _torch()
+        self._bind_stream()
+        H = self._dev(H, torch.float64)
+        P = self._dev(P, torch.float64)
+        nlev, nch = P.shape
+        ldw = nlev + (nlev & 1)
+        Ek = torch.empty(nlev, dtype=torch.float64, device=H.device)
+        w = torch.zeros((nch, ldw), dtype=torch.float64, device=H.device)
+        self._check(self.lib.rmx_inner_region(self._h, _ptr(H), nlev, _ptr(P), nch, _ptr(Ek), _ptr(w),
+                                              ldw), "rmx_inner_region")
+        return Ek, w, nlev, ldw
+
     # ------------------------------------------------------------------ post-processing
     def convolve_gaussian(self, x, dE: float, fwhm: float, mix=None):
         """rmx_convolve_gaussian: x [nspec, ne] (or [ne]) on a uniform mesh of spacing dE ->
@@ -403,6 +421,10 @@ def rmx_sweep(w, Ek, a, E, F, G, Fp, Gp, n_open=None, batch=0, dump_idx=None):
 def rmx_collision_strength_levels(K, level_start, g=1.0, n_open=None, omega=None, status=None):
     return _ctx().collision_strength_levels(K, level_start, g=g, n_open=n_open, omega=omega,
                                             status=status)
+
+
+def rmx_inner_region(H, P):
+    return _ctx().inner_region(H, P)
 
 
 def rmx_convolve_gaussian(x, dE, fwhm, mix=None):

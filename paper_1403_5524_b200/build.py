@@ -18,6 +18,8 @@ HEADERS = ["rmx_common.cuh", "cta_la.cuh", "rmx_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared"]
+# cuSOLVER (syevd) + cuBLAS (one DGEMM) serve only the inner-region eigensolve (NEXT-3)
+LIBS = ["-L/usr/local/cuda/lib64", "-lcusolver", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def _stale() -> bool:
@@ -34,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+    cmd = [NVCC, *FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd, cwd=CSRC)

@@ -7,6 +7,9 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
 #include "rmx_internal.h"
 
 using namespace rmx;
@@ -39,6 +42,10 @@ struct rmx_ctx {
   } dw, dEk, dE, dF, dG, dFp, dGp, dno, drs, dst;
   // post-processing scratch (NEXT-4): Gaussian weight table, admixture weights, Maxwell partials
   Dev dgt, dmix, dpart;
+  // inner-region eigensolve (NEXT-3): library handles (created on first use) and scratch
+  cusolverDnHandle_t solver = nullptr;
+  cublasHandle_t blas = nullptr;
+  Dev dV, dwork, dinfo;
   // instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> free_events;
@@ -222,8 +229,10 @@ rmx_rc rmx_destroy(rmx_ctx *c) {
   cudaFree(c->match_views);
   cudaFree(c->tepi_views);
   for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
-                  &c->dst})
+                  &c->dst, &c->dgt, &c->dmix, &c->dpart, &c->dV, &c->dwork, &c->dinfo})
     cudaFree(d->p);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->blas) cublasDestroy(c->blas);
   delete c;
   return RMX_OK;
 }
@@ -554,6 +563,64 @@ rmx_rc rmx_maxwell_average(rmx_ctx *c, const double *omega, int64_t ne, int64_t 
                           static_cast<double *>(c->dpart.p), ups, c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_maxwell_average");
+  return RMX_OK;
+}
+
+rmx_rc rmx_inner_region(rmx_ctx *c, const double *H, int64_t nlev, const double *P, int64_t nch,
+                        double *Ek, double *w, int64_t ldw) {
+  if (!c) return RMX_EINVAL;
+  if (!H || !P || !Ek || !w) return fail(c, RMX_EINVAL, "rmx_inner_region: null pointer");
+  if (nlev < 1 || nch < 1 || nlev > (1 << 17)) return fail(c, RMX_EINVAL, "rmx_inner_region: bad sizes");
+  if (ldw < nlev) return fail(c, RMX_EINVAL, "rmx_inner_region: ldw < nlev");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  if (!c->solver && cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS)
+    return fail(c, RMX_ECUDA, "rmx_inner_region: cusolverDnCreate failed");
+  if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
+    return fail(c, RMX_ECUDA, "rmx_inner_region: cublasCreate failed");
+  cusolverDnSetStream(c->solver, c->stream);
+  cublasSetStream(c->blas, c->stream);
+  const size_t nn = static_cast<size_t>(nlev) * nlev;
+  rmx_rc rc;
+  if ((rc = grow(c, c->dV, sizeof(double) * nn)) || (rc = grow(c, c->dinfo, sizeof(int))))
+    return rc;
+  double *V = static_cast<double *>(c->dV.p);
+  cudaError_t e = cudaMemcpyAsync(V, H, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_inner_region/copy");
+  // H is symmetric, so its row-major array is also its column-major array; after syevd the
+  // column-major V holds eigenvector k in column k (= row k of the row-major view), E_k ascending.
+  const int n = static_cast<int>(nlev);
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, V, n,
+                                  Ek, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return fail(c, RMX_ECUDA, "rmx_inner_region: syevd_bufferSize failed");
+  if ((rc = grow(c, c->dwork, sizeof(double) * static_cast<size_t>(lwork)))) return rc;
+  int *info = static_cast<int *>(c->dinfo.p);
+  cusolverStatus_t ss;
+  e = timed(c, RMX_KID_OTHER, 1, [&] {
+    ss = cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, V, n, Ek,
+                          static_cast<double *>(c->dwork.p), lwork, info);
+    return cudaGetLastError();
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_inner_region/syevd");
+  if (ss != CUSOLVER_STATUS_SUCCESS) return fail(c, RMX_ECUDA, "rmx_inner_region: syevd failed");
+  // w = P^T V, written row-major [nch][ldw]: as column-major that is w_cm (nlev x nch, ld ldw)
+  // = V^T P, with P's row-major [nlev][nch] array being the column-major nch x nlev matrix P^T.
+  const double one = 1.0, zero = 0.0;
+  cublasStatus_t bs;
+  e = timed(c, RMX_KID_OTHER, 1, [&] {
+    bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_T, n, static_cast<int>(nch), n, &one, V, n, P,
+                     static_cast<int>(nch), &zero, w, static_cast<int>(ldw));
+    return cudaGetLastError();
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_inner_region/gemm");
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(c, RMX_ECUDA, "rmx_inner_region: cublasDgemm failed");
+  int hinfo = 0;
+  e = cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  e = e ? e : cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_inner_region/info");
+  if (hinfo != 0)
+    return fail(c, RMX_ECUDA, "rmx_inner_region: syevd info = " + std::to_string(hinfo));
   return RMX_OK;
 }
 
