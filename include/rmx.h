@@ -189,6 +189,51 @@ rmx_rc rmx_sweep_host(rmx_ctx *ctx, const double *w, int64_t ldw, const double *
                       const int32_t *n_open, int64_t batch, double *rowsum, int32_t *status,
                       int64_t *h2d_bytes, int64_t *d2h_bytes);
 
+/* ---- NEXT-1 of SURVEY.md §8(f): the photoionisation variant of the sweep ------------------- *
+ * PAPER.md:116-122, 148-156 (the bound-free dipole outer region PSTGBF0DAMP whose sweeps Tables 1-2
+ * time). The paper prints no formula; readings P1-P4 give the R-matrix one used here:
+ *   (9)  g_i(E) = sum_k w_ik d_k / (E_k - E)          d_k = <psi_k|D|Psi_0>, inner-region dipoles
+ *   (10) v_j    = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij), j < n_open   ((1/2) U'^T g, U = F + G K)
+ *   (11) M      = (I - i K_oo)^{-1} v                  (ingoing-wave final states)
+ *   (12) sigma  = C (E - E0) sum_j |M_j|^2            (C = 4 pi^2 alpha / 3 in atomic units)
+ */
+
+/*
+ * rmx_dipole_amplitude - step (9) for ne energies: an energy-batched FP64 contraction with the
+ * operand d_k/(E_k - E) generated on chip.
+ *   w DEVICE [nch][ldw] (ldw >= nlev), Ek DEVICE [nlev], d DEVICE [nlev], E DEVICE [ne],
+ *   g DEVICE [ne][nch] output, status DEVICE int32 [ne] or NULL (RMX_E_POLE, g = NaN, as build_R).
+ */
+rmx_rc rmx_dipole_amplitude(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek,
+                            const double *d, int64_t nch, int64_t nlev, const double *E, int64_t ne,
+                            double *g, int32_t *status);
+
+/*
+ * rmx_photoionization - steps (10)-(12) from K (rmx_match_K output, all rows, closed columns -e_j)
+ * and g: v, then M by the real SPD route y = (I + K_oo^2)^{-1} v, M = y + i K_oo y (K_oo symmetric,
+ * reading M1), per-channel |M_j|^2 and sigma.
+ *   K DEVICE [ne][nch][nch]; g, Fp, Gp DEVICE [ne][nch]; E DEVICE [ne]; n_open DEVICE int32 [ne] or NULL
+ *   E0     initial (bound) state energy: photon energy = E - E0
+ *   C      cross-section prefactor (e.g. 4 pi^2 alpha / 3 = 0.0960769... in atomic units)
+ *   sigma  DEVICE [ne] output;  mabs2 DEVICE [ne][nch] or NULL (|M_j|^2, 0 for closed channels)
+ *   status DEVICE int32 [ne] or NULL: RMX_E_NONFINITE if |M|^2 is not finite
+ */
+rmx_rc rmx_photoionization(rmx_ctx *ctx, const double *K, const double *g, const double *Fp,
+                           const double *Gp, const double *E, int64_t nch, int64_t ne,
+                           const int32_t *n_open, double E0, double C, double *sigma,
+                           double *mabs2, int32_t *status);
+
+/*
+ * rmx_sweep_photo - the fused photoionisation sweep: per batch R -> K (as rmx_sweep), g, then the
+ * T-route Cholesky with v as one extra right-hand side; only sigma [ne] (and optionally
+ * mabs2 [ne][nch]) and status leave the device. Arguments as rmx_sweep plus d, E0, C.
+ */
+rmx_rc rmx_sweep_photo(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek, const double *d,
+                       int64_t nch, int64_t nlev, double a, const double *E, int64_t ne,
+                       const double *F, const double *G, const double *Fp, const double *Gp,
+                       const int32_t *n_open, int64_t batch, double E0, double C, double *sigma,
+                       double *mabs2, int32_t *status);
+
 /* ---- NEXT-3 of SURVEY.md §8(f): the inner-region step that feeds the sweep ------------------ */
 
 /*

@@ -50,8 +50,10 @@ def _load():
             lib.oracle_T2.argtypes = [P, i64, i64, P, P, P, P, P, i32]
             lib.oracle_sweep.argtypes = [P, i64, P, i64, i64, d, P, P, P, P, P, P, P, i64,
                                          P, P, P, P, P, P, i32]
+            lib.oracle_dipole_g.argtypes = [P, i64, P, P, i64, i64, d, P]
+            lib.oracle_photo.argtypes = [P, i64, i64, P, P, P, P, P, P]
             for f in (lib.oracle_R, lib.oracle_R_entries, lib.oracle_K, lib.oracle_T2,
-                      lib.oracle_sweep, lib.oracle_max_threads):
+                      lib.oracle_sweep, lib.oracle_max_threads, lib.oracle_dipole_g, lib.oracle_photo):
                 f.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -211,3 +213,50 @@ def inner_region(H, P):
     (LAPACK via numpy - a library primitive used as the step), w = P^T V. Returns (Ek, w [nch, nlev])."""
     Ek, V = np.linalg.eigh(np.asarray(H, dtype=np.float64))
     return Ek, np.ascontiguousarray(np.asarray(P, dtype=np.float64).T @ V)
+
+
+FINE_STRUCTURE_ALPHA = 1.0 / 137.035999084  # CODATA 2018
+SIGMA_PREFACTOR = 4.0 * np.pi ** 2 * FINE_STRUCTURE_ALPHA / 3.0  # DESIGN.md reading P4 (a.u.)
+
+
+def dipole_g(w, Ek, d, E):
+    """NEXT-1 step (9): g_i(E) = sum_k w_ik d_k/(E_k - E) (the outer-region dipole amplitude
+    contraction of SURVEY.md §8(f) item 1). Returns (g [nch], status)."""
+    w, Ek, d = _f64(w), _f64(Ek), _f64(d)
+    nch, nlev = w.shape
+    g = np.empty(nch)
+    st = _load().oracle_dipole_g(_p(w), nlev, _p(Ek), _p(d), nch, nlev, float(E), _p(g))
+    return g, st
+
+
+def photo(K_, n_open: int, g, Fp, Gp):
+    """NEXT-1 steps (10)-(11): v = (1/2) U'^T g over the open solutions, (I - iK_oo) M = v by
+    complex GE. Returns (M complex [n_open], |M_j|^2 [nch] (0 on closed channels), status)."""
+    K_ = _f64(K_)
+    n = K_.shape[0]
+    g, Fp, Gp = _f64(g), _f64(Fp), _f64(Gp)
+    mr, mi, m2 = np.zeros(max(n_open, 1)), np.zeros(max(n_open, 1)), np.empty(n)
+    st = _load().oracle_photo(_p(K_), n, int(n_open), _p(g), _p(Fp), _p(Gp), _p(mr), _p(mi), _p(m2))
+    return (mr + 1j * mi)[:n_open], m2, st
+
+
+def photo_sweep(w, Ek, d, a, E, F, G, Fp, Gp, n_open, E0, C=SIGMA_PREFACTOR, threads=None):
+    """NEXT-1 end to end on each energy of E: R (2) -> K (4) -> g (9) -> M (10-11) ->
+    sigma = C (E - E0) sum_j |M_j|^2 (12). Returns dict(sigma [ne], mabs2 [ne, nch], g [ne, nch],
+    status [ne])."""
+    E = _f64(E)
+    ne = len(E)
+    nch = np.asarray(w).shape[0]
+    no = np.asarray(n_open, dtype=np.int32)
+    ks = sweep(w, Ek, a, E, F, G, Fp, Gp, no, np.arange(ne), want=("K",), threads=threads)
+    out = {"sigma": np.empty(ne), "mabs2": np.empty((ne, nch)), "g": np.empty((ne, nch)),
+           "status": ks["status"].copy()}
+    for e in range(ne):
+        g, st = dipole_g(w, Ek, d, E[e])
+        M, m2, st2 = photo(ks["K"][e], int(no[e]), g, Fp[e], Gp[e])
+        out["g"][e], out["mabs2"][e] = g, m2
+        out["sigma"][e] = float(np.longdouble(C) * (np.longdouble(E[e]) - np.longdouble(E0)) *
+                                np.sum(m2.astype(np.longdouble)))
+        if out["status"][e] == 0:
+            out["status"][e] = st or st2
+    return out

@@ -24,6 +24,14 @@
  *   (7) |T_ij|^2 = Re^2 + Im^2 on the open block, 0 elsewhere; rowsum_i = sum_j |T_ij|^2
  *   (8) diagnostics    : unitarity max|S S^H - I| with S = I + T; max|K_oo - K_oo^T|; cond_1(A)
  *
+ * NEXT-1 (photoionisation variant; DESIGN.md
+ * readings P1-P4), per energy, after (4):
+ *   (9)  g_i(E)  = sum_k w_ik d_k / (E_k - E)    (dipole amplitude contraction, ascending k)
+ *   (10) v_j     = (1/2) (g_j F'_j + sum_i g_i G'_i K_ij),  j < n_o   (v = (1/2) U'^T g with the
+ *                  standing-wave solutions U = F + G K of (4), derivatives at r = a)
+ *   (11) (I - i K_oo) M = v by complex long double GE (ingoing-wave normalisation U (I - iK_oo)^-1)
+ *   (12) |M_j|^2; sigma(E) = C (E - E0) sum_j |M_j|^2 (in oracle/__init__.py)
+ *
  * Parallelism (OpenMP) only splits independent rows / energies; each output element sees
  * the same operation sequence for any thread count, so results are thread-count invariant.
  *
@@ -236,6 +244,68 @@ static int t_matrix_cld(const ld *K, int64_t n, int64_t o, cld *T, double *unita
       }
     *unitarity = (double)worst;
   }
+  free(M);
+  return st;
+}
+
+/* ---- (9)-(11) photoionisation amplitudes (NEXT-1) ------------------------------------ */
+
+/* g[nch] = sum_k w_ik d_k / (E_k - E) in long double, ascending k. */
+static int dipole_g_ld(const double *w, int64_t ldw, const double *Ek, const double *d, int64_t nch,
+                       int64_t nlev, double E, ld *g) {
+  for (int64_t k = 0; k < nlev; ++k)
+    if (fabsl((ld)Ek[k] - (ld)E) < POLE_GUARD) return ORC_POLE;
+  for (int64_t i = 0; i < nch; ++i) {
+    ld s = 0.0L;
+    for (int64_t k = 0; k < nlev; ++k) s += (ld)w[i * ldw + k] * ((ld)d[k] / ((ld)Ek[k] - (ld)E));
+    g[i] = s;
+  }
+  return ORC_OK;
+}
+
+/* K: full nch*nch (double, row-major, closed columns -e_j); M (complex, o entries) and |M|^2. */
+static int photo_amp_ld(const double *K, int64_t n, int64_t o, const ld *g, const double *Fp,
+                        const double *Gp, cld *M) {
+  if (o == 0) return ORC_OK;
+  cld *A = (cld *)malloc(sizeof(cld) * (size_t)o * (size_t)o);
+  for (int64_t j = 0; j < o; ++j) {
+    ld s = g[j] * (ld)Fp[j];
+    for (int64_t i = 0; i < n; ++i) s += g[i] * (ld)Gp[i] * (ld)K[i * n + j];
+    M[j] = 0.5L * s;                                                   /* v_j */
+    for (int64_t l = 0; l < o; ++l)
+      A[j * o + l] = (j == l ? 1.0L : 0.0L) - I * (ld)K[j * n + l];    /* I - iK_oo */
+  }
+  int st = ge_solve_cld(A, M, o, 1, 1);
+  free(A);
+  return st;
+}
+
+int oracle_dipole_g(const double *w, int64_t ldw, const double *Ek, const double *d, int64_t nch,
+                    int64_t nlev, double E, double *g) {
+  ld *gl = (ld *)malloc(sizeof(ld) * (size_t)nch);
+  int st = dipole_g_ld(w, ldw, Ek, d, nch, nlev, E, gl);
+  for (int64_t i = 0; i < nch; ++i) g[i] = st == ORC_OK ? (double)gl[i] : NAN;
+  free(gl);
+  return st;
+}
+
+/* M_re/M_im [n_open], mabs2 [nch] (0 for closed channels). g is taken in double (as stored). */
+int oracle_photo(const double *K, int64_t nch, int64_t n_open, const double *g, const double *Fp,
+                 const double *Gp, double *M_re, double *M_im, double *mabs2) {
+  ld *gl = (ld *)malloc(sizeof(ld) * (size_t)nch);
+  cld *M = (cld *)malloc(sizeof(cld) * (size_t)(n_open > 0 ? n_open : 1));
+  for (int64_t i = 0; i < nch; ++i) gl[i] = g[i];
+  int st = photo_amp_ld(K, nch, n_open, gl, Fp, Gp, M);
+  for (int64_t j = 0; j < nch; ++j) {
+    if (j < n_open) {
+      M_re[j] = (double)creall(M[j]);
+      M_im[j] = (double)cimagl(M[j]);
+      mabs2[j] = (double)(creall(M[j]) * creall(M[j]) + cimagl(M[j]) * cimagl(M[j]));
+    } else {
+      mabs2[j] = 0.0;
+    }
+  }
+  free(gl);
   free(M);
   return st;
 }

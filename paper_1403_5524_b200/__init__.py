@@ -32,7 +32,8 @@ KID_NAMES = ("rform", "match", "tepi", "other")
 # every symbol include/rmx.h declares (tests/test_abi.py checks the header and the .so agree)
 EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rmx_build_R",
             "rmx_match_K", "rmx_collision_strength", "rmx_collision_strength_levels", "rmx_sweep",
-            "rmx_sweep_levels", "rmx_sweep_host", "rmx_inner_region", "rmx_convolve_gaussian",
+            "rmx_sweep_levels", "rmx_sweep_host", "rmx_dipole_amplitude", "rmx_photoionization",
+            "rmx_sweep_photo", "rmx_inner_region", "rmx_convolve_gaussian",
             "rmx_maxwell_average",
             "rmx_sync",
             "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version", "rmx_sm_target")
@@ -68,6 +69,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                              P],
         "rmx_sweep_host": [P, P, i64, P, i64, i64, d, P, i64, P, P, P, P, P, i64, P, P, P, P],
         "rmx_inner_region": [P, P, i64, P, i64, P, P, i64],
+        "rmx_dipole_amplitude": [P, P, i64, P, P, i64, i64, P, i64, P, P],
+        "rmx_photoionization": [P, P, P, P, P, P, i64, i64, P, d, d, P, P, P],
+        "rmx_sweep_photo": [P, P, i64, P, P, i64, i64, d, P, i64, P, P, P, P, P, i64, d, d, P, P, P],
         "rmx_convolve_gaussian": [P, P, i64, P, i64, d, d, P],
         "rmx_maxwell_average": [P, P, i64, i64, P, P, P, i64, P],
         "rmx_sync": [P, P, i64, P],
@@ -309,6 +313,62 @@ class Context:
             "rmx_sweep_host")
         return rowsum, status, h2d.value, d2h.value
 
+    # ------------------------------------------------------------------ photoionisation (NEXT-1)
+    SIGMA_PREFACTOR = 4.0 * np.pi ** 2 / 137.035999084 / 3.0  # 4 pi^2 alpha / 3 (atomic units)
+
+    def dipole_amplitude(self, w, Ek, d, E, status=None):
+        """rmx_dipole_amplitude: g[e][i] = sum_k w_ik d_k/(E_k - E_e). Returns (g [ne,nch], status)."""
+        torch = _torch()
+        self._bind_stream()
+        w, nlev, ldw = self.prepare_w(w)
+        Ek, d, E = (self._dev(x, torch.float64) for x in (Ek, d, E))
+        nch, ne = w.shape[0], E.shape[0]
+        g = torch.empty((ne, nch), dtype=torch.float64, device=w.device)
+        status = self._status(status, ne)
+        self._check(self.lib.rmx_dipole_amplitude(self._h, _ptr(w), ldw, _ptr(Ek), _ptr(d), nch, nlev,
+                                                  _ptr(E), ne, _ptr(g), _ptr(status)),
+                    "rmx_dipole_amplitude")
+        return g, status
+
+    def photoionization(self, K, g, Fp, Gp, E, E0: float, C: Optional[float] = None, n_open=None,
+                        status=None, want_mabs2: bool = True):
+        """rmx_photoionization: sigma(E) = C (E - E0) sum_j |M_j|^2, M = (I - iK_oo)^{-1} (1/2) U'^T g.
+        Returns (sigma [ne], mabs2 [ne,nch] or None, status)."""
+        torch = _torch()
+        self._bind_stream()
+        K = self._dev(K, torch.float64)
+        g, Fp, Gp, E = (self._dev(x, torch.float64) for x in (g, Fp, Gp, E))
+        ne, nch = K.shape[0], K.shape[1]
+        no = None if n_open is None else self._dev(n_open, torch.int32)
+        sigma = torch.empty(ne, dtype=torch.float64, device=K.device)
+        m2 = torch.empty((ne, nch), dtype=torch.float64, device=K.device) if want_mabs2 else None
+        status = self._status(status, ne)
+        C = self.SIGMA_PREFACTOR if C is None else float(C)
+        self._check(self.lib.rmx_photoionization(self._h, _ptr(K), _ptr(g), _ptr(Fp), _ptr(Gp), _ptr(E),
+                                                 nch, ne, _ptr(no), float(E0), C, _ptr(sigma), _ptr(m2),
+                                                 _ptr(status)), "rmx_photoionization")
+        return sigma, m2, status
+
+    def sweep_photo(self, w, Ek, d, a: float, E, F, G, Fp, Gp, n_open, E0: float,
+                    C: Optional[float] = None, batch: int = 0, status=None, want_mabs2: bool = False):
+        """rmx_sweep_photo: fused R -> K -> g -> sigma for all energies. Returns dict(sigma, mabs2, status)."""
+        torch = _torch()
+        self._bind_stream()
+        w, nlev, ldw = self.prepare_w(w)
+        Ek, d, E = (self._dev(x, torch.float64) for x in (Ek, d, E))
+        F, G, Fp, Gp = (self._dev(x, torch.float64) for x in (F, G, Fp, Gp))
+        n_open = None if n_open is None else self._dev(n_open, torch.int32)
+        nch, ne = w.shape[0], E.shape[0]
+        sigma = torch.empty(ne, dtype=torch.float64, device=w.device)
+        m2 = torch.empty((ne, nch), dtype=torch.float64, device=w.device) if want_mabs2 else None
+        status = self._status(status, ne)
+        C = self.SIGMA_PREFACTOR if C is None else float(C)
+        self._check(self.lib.rmx_sweep_photo(
+            self._h, _ptr(w), ldw, _ptr(Ek), _ptr(d), nch, nlev, float(a), _ptr(E), ne, _ptr(F), _ptr(G),
+            _ptr(Fp), _ptr(Gp), _ptr(n_open), int(batch), float(E0), C, _ptr(sigma), _ptr(m2),
+            _ptr(status)), "rmx_sweep_photo")
+        return {"sigma": sigma, "mabs2": m2, "status": status}
+
     # ------------------------------------------------------------------ inner region (NEXT-3)
     def inner_region(self, H, P):
         """rmx_inner_region: (E_k, V) = eigh(H), w = P^T V. Returns (Ek [nlev], w [nch, ldw], nlev,
@@ -421,6 +481,18 @@ def rmx_sweep(w, Ek, a, E, F, G, Fp, Gp, n_open=None, batch=0, dump_idx=None):
 def rmx_collision_strength_levels(K, level_start, g=1.0, n_open=None, omega=None, status=None):
     return _ctx().collision_strength_levels(K, level_start, g=g, n_open=n_open, omega=omega,
                                             status=status)
+
+
+def rmx_dipole_amplitude(w, Ek, d, E, status=None):
+    return _ctx().dipole_amplitude(w, Ek, d, E, status=status)
+
+
+def rmx_photoionization(K, g, Fp, Gp, E, E0, C=None, n_open=None, status=None):
+    return _ctx().photoionization(K, g, Fp, Gp, E, E0, C=C, n_open=n_open, status=status)
+
+
+def rmx_sweep_photo(w, Ek, d, a, E, F, G, Fp, Gp, n_open, E0, C=None, batch=0):
+    return _ctx().sweep_photo(w, Ek, d, a, E, F, G, Fp, Gp, n_open, E0, C=C, batch=batch)
 
 
 def rmx_inner_region(H, P):

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(CONV_TILE) conv_gauss_kernel(const double *__r
   extern __shared__ double sm[];
   double *xs = sm;                        // [CONV_TILE + 2M]
   double *gs = sm + CONV_TILE + 2 * M;    // [M + 1]
+  __shared__ double gfull;                // g_0 + 2 sum_d g_d: the interior normalisation
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * CONV_TILE;
   const int spec = blockIdx.y;  // output spectrum (0 when mixing)
   for (int d = threadIdx.x; d <= M; d += blockDim.x) gs[d] = gtab[d];
@@ -66,16 +67,20 @@ __global__ void __launch_bounds__(CONV_TILE) conv_gauss_kernel(const double *__r
     xs[q] = v;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int d = M; d >= 1; --d) t += gs[d];
+    gfull = gs[0] + 2.0 * t;
+  }
+  __syncthreads();
   const int64_t i = i0 + threadIdx.x;
   if (i >= ne) return;
   const double *xc = xs + threadIdx.x + M;  // x_i
   double num = gs[0] * xc[0], den = gs[0];
   const bool interior = (i - M >= 0) && (i + M < ne);
-  if (interior) {
-    for (int d = 1; d <= M; ++d) {
-      num = fma(gs[d], xc[-d] + xc[d], num);
-      den += 2.0 * gs[d];
-    }
+  if (interior) {  // symmetric window: one add + one FMA per pair (j = i -+ d)
+    for (int d = 1; d <= M; ++d) num = fma(gs[d], xc[-d] + xc[d], num);
+    den = gfull;
   } else {
     for (int d = 1; d <= M; ++d) {
       const double gd = gs[d];

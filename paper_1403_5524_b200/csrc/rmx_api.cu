@@ -46,6 +46,8 @@ struct rmx_ctx {
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   Dev dV, dwork, dinfo;
+  // photoionisation amplitudes g of one sweep batch (NEXT-1)
+  Dev dg;
   // instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> free_events;
@@ -229,7 +231,7 @@ rmx_rc rmx_destroy(rmx_ctx *c) {
   cudaFree(c->match_views);
   cudaFree(c->tepi_views);
   for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
-                  &c->dst, &c->dgt, &c->dmix, &c->dpart, &c->dV, &c->dwork, &c->dinfo})
+                  &c->dst, &c->dgt, &c->dmix, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg})
     cudaFree(d->p);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->blas) cublasDestroy(c->blas);
@@ -304,7 +306,7 @@ rmx_rc rmx_collision_strength(rmx_ctx *c, const double *K, int64_t nch, int64_t 
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
-    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, LevelSums{}, c->ws,
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, T2, nullptr, rowsum, LevelSums{}, PhotoArgs{}, c->ws,
                        ws_slot_doubles(nch), c->tepi_views, slots, status, c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_collision_strength");
@@ -340,7 +342,7 @@ rmx_rc rmx_collision_strength_levels(rmx_ctx *c, const double *K, int64_t nch, i
   lv.g = g;
   lv.omega = omega;
   cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
-    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, nullptr, nullptr, nullptr, lv, c->ws,
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, nullptr, nullptr, nullptr, lv, PhotoArgs{}, c->ws,
                        ws_slot_doubles(nch), c->tepi_views, slots, status, c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_collision_strength_levels");
@@ -355,14 +357,21 @@ static int64_t default_batch(const rmx_ctx *c, int64_t nch, int64_t ne) {
   return std::min<int64_t>(b, ne);
 }
 
+// NEXT-1 inputs/outputs of the fused photoionisation sweep
+struct PhotoIn {
+  const double *d;
+  double E0, C;
+  double *sigma, *mabs2;
+};
+
 static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
                          int64_t nlev, double a, const double *E, int64_t ne, const double *F,
                          const double *G, const double *Fp, const double *Gp,
                          const int32_t *n_open, int64_t batch, const int64_t *dump_idx,
                          int64_t n_dump, double *R_d, double *K_d, double *T2_d, double *rowsum,
-                         const LevelSums &lv, int32_t *status) {
+                         const LevelSums &lv, int32_t *status, const PhotoIn *ph = nullptr) {
   if (!c) return RMX_EINVAL;
-  if (!w || !Ek || !E || !F || !G || !Fp || !Gp || (!rowsum && !lv.omega))
+  if (!w || !Ek || !E || !F || !G || !Fp || !Gp || (!rowsum && !lv.omega && !ph))
     return fail(c, RMX_EINVAL, "rmx_sweep: null pointer");
   if (nch < 1 || nlev < 1 || ne < 1) return fail(c, RMX_EINVAL, "rmx_sweep: sizes must be >= 1");
   if (nch > kMaxMatchChannels)
@@ -386,6 +395,7 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
             static_cast<size_t>(batch) * mat * sizeof(double));
   if (rc != RMX_OK) return rc;
   double *rb = c->rbuf;
+  if (ph && (rc = grow(c, c->dg, sizeof(double) * batch * nch))) return rc;
   std::string err;
   for (int64_t b0 = 0; b0 < ne; b0 += batch) {
     const int64_t nb = std::min(batch, ne - b0);
@@ -413,16 +423,33 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
       if (T2_d) {
         e = timed(c, RMX_KID_TEPI, 1, [&] {
           return launch_tepi(rb + l * mat, nch, mat, nch, 1, nob ? nob + l : nullptr, T2_d + d * mat,
-                             nullptr, nullptr, LevelSums{}, c->ws, ws_slot_doubles(nch), c->tepi_views, 1, nullptr, c->stream);
+                             nullptr, nullptr, LevelSums{}, PhotoArgs{}, c->ws, ws_slot_doubles(nch), c->tepi_views, 1, nullptr, c->stream);
         });
         if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T dump");
       }
     }
     LevelSums lvb = lv;
     if (lvb.omega) lvb.omega += b0 * static_cast<int64_t>(lv.nlevel) * lv.nlevel;
+    PhotoArgs pab;
+    if (ph) {
+      // NEXT-1: g for this batch, then the amplitudes inside the T epilogue
+      double *gb = static_cast<double *>(c->dg.p);
+      e = timed(c, RMX_KID_OTHER, 1, [&] {
+        return launch_dipole_g(w, ldw, Ek, ph->d, nch, nlev, E + b0, nb, gb, stb, c->stream);
+      });
+      if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep_photo/g");
+      pab.g = gb;
+      pab.Fp = Fp + b0 * nch;
+      pab.Gp = Gp + b0 * nch;
+      pab.E = E + b0;
+      pab.E0 = ph->E0;
+      pab.C = ph->C;
+      pab.sigma = ph->sigma + b0;
+      pab.mabs2 = ph->mabs2 ? ph->mabs2 + b0 * nch : nullptr;
+    }
     e = timed(c, RMX_KID_TEPI, 1, [&] {
       return launch_tepi(rb, nch, mat, nch, nb, nob, nullptr, nullptr,
-                         rowsum ? rowsum + b0 * nch : nullptr, lvb, c->ws, ws_slot_doubles(nch),
+                         rowsum ? rowsum + b0 * nch : nullptr, lvb, pab, c->ws, ws_slot_doubles(nch),
                          c->tepi_views, slots, stb, c->stream);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/T");
@@ -456,6 +483,66 @@ rmx_rc rmx_sweep_levels(rmx_ctx *c, const double *w, int64_t ldw, const double *
   lv.omega = omega;
   return sweep_impl(c, w, ldw, Ek, nch, nlev, a, E, ne, F, G, Fp, Gp, n_open, batch, nullptr, 0,
                     nullptr, nullptr, nullptr, rowsum, lv, status);
+}
+
+rmx_rc rmx_dipole_amplitude(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek,
+                            const double *d, int64_t nch, int64_t nlev, const double *E, int64_t ne,
+                            double *g, int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!w || !Ek || !d || !E || !g) return fail(c, RMX_EINVAL, "rmx_dipole_amplitude: null pointer");
+  if (nch < 1 || nlev < 1 || ne < 1 || nch > (1 << 20) || nlev > (1 << 30))
+    return fail(c, RMX_EINVAL, "rmx_dipole_amplitude: bad sizes");
+  if (ldw < nlev) return fail(c, RMX_EINVAL, "rmx_dipole_amplitude: ldw < nlev");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  cudaError_t e = timed(c, RMX_KID_OTHER, 1, [&] {
+    return launch_dipole_g(w, ldw, Ek, d, nch, nlev, E, ne, g, status, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_dipole_amplitude");
+  return RMX_OK;
+}
+
+rmx_rc rmx_photoionization(rmx_ctx *c, const double *K, const double *g, const double *Fp,
+                           const double *Gp, const double *E, int64_t nch, int64_t ne,
+                           const int32_t *n_open, double E0, double C, double *sigma,
+                           double *mabs2, int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!K || !g || !Fp || !Gp || !E || !sigma)
+    return fail(c, RMX_EINVAL, "rmx_photoionization: null pointer");
+  if (nch < 1 || ne < 1 || nch > kMaxMatchChannels)
+    return fail(c, RMX_EINVAL, "rmx_photoionization: bad sizes");
+  if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
+  cudaSetDevice(c->device);
+  const int64_t slots = ws_slots_for(c, ne);
+  rmx_rc rc = ensure_ws(c, nch, slots);
+  if (rc != RMX_OK) return rc;
+  PhotoArgs pa;
+  pa.g = g;
+  pa.Fp = Fp;
+  pa.Gp = Gp;
+  pa.E = E;
+  pa.E0 = E0;
+  pa.C = C;
+  pa.sigma = sigma;
+  pa.mabs2 = mabs2;
+  cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
+    return launch_tepi(K, nch, nch * nch, nch, ne, n_open, nullptr, nullptr, nullptr, LevelSums{}, pa,
+                       c->ws, ws_slot_doubles(nch), c->tepi_views, slots, status, c->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_photoionization");
+  return RMX_OK;
+}
+
+rmx_rc rmx_sweep_photo(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, const double *d,
+                       int64_t nch, int64_t nlev, double a, const double *E, int64_t ne,
+                       const double *F, const double *G, const double *Fp, const double *Gp,
+                       const int32_t *n_open, int64_t batch, double E0, double C, double *sigma,
+                       double *mabs2, int32_t *status) {
+  if (!c) return RMX_EINVAL;
+  if (!d || !sigma) return fail(c, RMX_EINVAL, "rmx_sweep_photo: null d / sigma");
+  PhotoIn ph{d, E0, C, sigma, mabs2};
+  return sweep_impl(c, w, ldw, Ek, nch, nlev, a, E, ne, F, G, Fp, Gp, n_open, batch, nullptr, 0,
+                    nullptr, nullptr, nullptr, nullptr, LevelSums{}, status, &ph);
 }
 
 rmx_rc rmx_sweep_host(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,

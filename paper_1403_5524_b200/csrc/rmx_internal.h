@@ -34,7 +34,7 @@ __host__ __device__ inline MatchLayout match_layout(int64_t nch) {
 }
 __host__ __device__ inline TepiLayout tepi_layout(int64_t nch) {
   TepiLayout L;
-  L.ldo = (nch + 1) & ~1LL;
+  L.ldo = (nch + 2) & ~1LL;  // >= nch + 1: room for the photoionisation right-hand side (column o)
   L.s_off = 0;
   L.x_off = nch * L.ldo + 32;
   L.k_off = L.x_off + nch * L.ldo + 32;
@@ -71,12 +71,25 @@ struct LevelSums {
   double g = 0.0;
   double *omega = nullptr;
 };
+// Optional photoionisation output of the T epilogue (NEXT-1, photo.cu header): per energy
+//   v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) (j < o), y = (I + K_oo^2)^{-1} v (the Cholesky factor
+//   of the T route), M = y + i K_oo y, mabs2_j = |M_j|^2, sigma = C (E - E0) sum_j |M_j|^2.
+// g == nullptr: off. g, Fp, Gp [ne][nch]; E [ne]; sigma [ne]; mabs2 [ne][nch] or nullptr.
+struct PhotoArgs {
+  const double *g = nullptr, *Fp = nullptr, *Gp = nullptr, *E = nullptr;
+  double E0 = 0.0, C = 0.0;
+  double *sigma = nullptr, *mabs2 = nullptr;
+};
 int64_t tepi_ws_doubles_per_slot(int64_t nch);
 void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs);
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
-                        const LevelSums &lv, double *ws, int64_t ws_slot, const CUtensorMap *views,
-                        int64_t ws_slots, int32_t *status, cudaStream_t st);
+                        const LevelSums &lv, const PhotoArgs &pa, double *ws, int64_t ws_slot,
+                        const CUtensorMap *views, int64_t ws_slots, int32_t *status, cudaStream_t st);
+// photo.cu
+cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, const double *d,
+                            int64_t nch, int64_t nlev, const double *E, int64_t ne, double *g,
+                            int32_t *status, cudaStream_t st);
 
 // post.cu (NEXT-4); the Gaussian window x[i-M, i+256+M) and its weights live in shared memory
 constexpr int kMaxConvHalfWidth = 9000;

@@ -58,7 +58,7 @@ __device__ __forceinline__ void mirror_lower(double *P, int64_t ld, int o, doubl
 __global__ void __launch_bounds__(NT, 1)
     tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
                 const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
-                double *rowsum, LevelSums lv, double *ws, int64_t ws_slot,
+                double *rowsum, LevelSums lv, PhotoArgs pa, double *ws, int64_t ws_slot,
                 const CUtensorMap *views, int32_t *status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TepiSmem &sm = *reinterpret_cast<TepiSmem *>(smem_raw);
@@ -102,6 +102,19 @@ __global__ void __launch_bounds__(NT, 1)
             }
         }
       }
+      if (pa.g) {
+        // NEXT-1 (10): v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) into X column o (the extra
+        // right-hand side of the solves below); gG_i staged in shared memory, i ascending
+        const double *ge = pa.g + e * n, *Fpe = pa.Fp + e * n, *Gpe = pa.Gp + e * n;
+        double *gG = sm.gemm;
+        for (int i = threadIdx.x; i < n; i += NT) gG[i] = ge[i] * Gpe[i];
+        __syncthreads();
+        for (int j = threadIdx.x; j < o; j += NT) {
+          double s = ge[j] * Fpe[j];
+          for (int i = 0; i < n; ++i) s = fma(gG[i], Ke[static_cast<int64_t>(i) * ldk + j], s);
+          *Xv.at(j, o) = 0.5 * s;
+        }
+      }
       __syncthreads();
       // S = I + K_oo K_oo^T (lower tiles)
       gemm_set(o, o, o, opk(Kv, 0, 0), opk(Kv, 0, 0), Sv, 0, 0, true, 1.0, smg, gs);
@@ -120,22 +133,23 @@ __global__ void __launch_bounds__(NT, 1)
                    smg, gs);
         }
       }
-      // forward: L Z = K  (X holds K_oo); X_p = L_pp^{-1} X_p (in place, one 128-row tile row)
+      // forward: L Z = K  (X holds K_oo [| v]); X_p = L_pp^{-1} X_p (in place, one 128-row tile row)
+      const int nr = o + (pa.g ? 1 : 0);  // right-hand sides
       for (int P0 = 0; P0 < o; P0 += NB) {
         const int W = min(NB, o - P0);
         tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
-        gemm_set(W, o, W, opk(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
+        gemm_set(W, nr, W, opk(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
         if (P0 + W < o)
-          gemm_sub(o - P0 - W, o, W, opk(Sv, P0 + W, P0), opn(Xv, P0, 0), Xv, P0 + W, 0, false, smg, gs);
+          gemm_sub(o - P0 - W, nr, W, opk(Sv, P0 + W, P0), opn(Xv, P0, 0), Xv, P0 + W, 0, false, smg, gs);
       }
       // backward: L^T X = Z; X_p = L_pp^{-T} X_p: A(i, k) = Tg[k][i]
       for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
         const int W = min(NB, o - P0);
         tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
-        gemm_set(W, o, W, opn(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
+        gemm_set(W, nr, W, opn(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
         if (P0 > 0)
           // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]
-          gemm_sub(P0, o, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
+          gemm_sub(P0, nr, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
       }
       // P = K_oo X = K S^{-1} K is symmetric: lower tiles only (half the flops), then mirrored
       gemm_set(o, o, o, opk(Kv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, true, 0.0, smg, gs);
@@ -169,6 +183,37 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (rowsum && lane_id() == 0) rowsum[e * n + i] = s;
+    }
+    if (pa.g) {
+      // NEXT-1 (11)-(12): y = X[:, o] = (I + K_oo^2)^{-1} v; M = y + i K_oo y; |M_j|^2; sigma.
+      // Row sums in a fixed order: warp w takes rows w, w + NW, ...; warps combined in order.
+      double *ys = sm.gemm, *wsum = sm.gemm + n + 1;
+      __syncthreads();
+      for (int j = threadIdx.x; j < o; j += NT) ys[j] = *Xv.at(j, o);
+      __syncthreads();
+      double part = 0.0;
+      for (int i = warp_id(); i < n; i += NW) {
+        double m2 = 0.0;
+        if (i < o) {
+          const double *kr = Kv.at(i, 0);
+          double t = 0.0;
+          for (int j = lane_id(); j < o; j += 32) t = fma(kr[j], ys[j], t);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+          m2 = fma(ys[i], ys[i], t * t);
+        }
+        if (!isfinite(m2)) bad = 1;
+        if (pa.mabs2 && lane_id() == 0) pa.mabs2[e * n + i] = m2;
+        part += m2;
+      }
+      if (lane_id() == 0) wsum[warp_id()] = part;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < NW; ++q) s += wsum[q];
+        pa.sigma[e] = pa.C * (pa.E[e] - pa.E0) * s;
+      }
+      __syncthreads();
     }
     if (lv.omega && o > 0) {
       // NEXT-2: level-pair collision strengths
@@ -207,8 +252,8 @@ void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
-                        const LevelSums &lv, double *ws, int64_t ws_slot, const CUtensorMap *views,
-                        int64_t ws_slots, int32_t *status, cudaStream_t st) {
+                        const LevelSums &lv, const PhotoArgs &pa, double *ws, int64_t ws_slot,
+                        const CUtensorMap *views, int64_t ws_slots, int32_t *status, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t ce = cudaFuncSetAttribute(tepi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -218,7 +263,7 @@ cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t n
   }
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
   tepi_kernel<<<grid, NT, sizeof(TepiSmem), st>>>(K, ldk, kstride, static_cast<int>(nch), ne, n_open,
-                                                  T2, t2_slot, rowsum, lv, ws, ws_slot, views, status);
+                                                  T2, t2_slot, rowsum, lv, pa, ws, ws_slot, views, status);
   return cudaGetLastError();
 }
 
