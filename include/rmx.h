@@ -272,8 +272,8 @@ rmx_rc rmx_inner_region(rmx_ctx *ctx, const double *H, int64_t nlev, const doubl
  *   mix  HOST [nspec] or NULL  admixture weights (>= 0, any scale: 2:1 == 2/3, 1/3)
  *   y    DEVICE [ne] if mix, else [nspec][ne]
  * Errors: EINVAL on null x/y, dE or fwhm <= 0, fwhm < 2 dE (SPEC.md:299 UnderResolvedKernel),
- * M > 9000, a negative weight or weights summing to 0. Async on the ctx stream (a call with mix
- * synchronises the stream before returning, since mix is read from the caller's host buffer).
+ * M > 9000, a negative weight or weights summing to 0, more than 64 admixture components.
+ * Async on the ctx stream (mix is read on the host during the call).
  */
 rmx_rc rmx_convolve_gaussian(rmx_ctx *ctx, const double *x, int64_t nspec, const double *mix,
                              int64_t ne, double dE, double fwhm, double *y);

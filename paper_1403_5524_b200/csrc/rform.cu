@@ -14,17 +14,22 @@
 //   * epilogue scales by 1/2a and stores the tile and its mirror image: R is bitwise symmetric.
 #include "rmx_common.cuh"
 #include "rmx_internal.h"
+#include <cstdlib>
 
 namespace rmx {
 
-template <int BM_, int STAGES_>
+template <int BM_, int STAGES_, bool PRODUCER_ = true>
 struct RformCfg {
   static constexpr int BM = BM_, STAGES = STAGES_;
+  // PRODUCER: a dedicated TMA/denominator warp (9 warps: 3 on one SM sub-partition caps the
+  // register file at 168 per thread and the pair mode spills); otherwise the consumer warps refill
+  // the ring in turn (8 warps, up to 255 registers, no spills).
+  static constexpr bool PRODUCER = PRODUCER_;
   static constexpr int BK = 32;    // k per pipeline stage
   static constexpr int BOXK = 16;  // doubles per TMA box row (128 B = swizzle span)
   static constexpr int NB = BM / 32;                       // 32 x 32 blocks per tile dimension
   static constexpr int NCW = (NB * NB / 2 > 4) ? NB * NB / 2 : 4;  // consumer warps, <= 2 blocks each
-  static constexpr int NT = (NCW + 1) * 32;
+  static constexpr int NT = (NCW + (PRODUCER ? 1 : 0)) * 32;
   static constexpr int BOX_BYTES = BM * BOXK * 8;
   static constexpr int OP_BYTES = 2 * BOX_BYTES;   // one operand, one stage
   static constexpr int STAGE_BYTES = 2 * OP_BYTES;  // tile I + tile J
@@ -139,6 +144,40 @@ __device__ __forceinline__ void rform_slab(double (&acc)[2][4][4][2], uint32_t a
   }
 }
 
+// Fill ring slot s with k-slab kt: d_k = 1/(E_k - E) for the slab's 32 k (one per lane) + pole guard,
+// then (lane 0) expect-tx and the 2 or 4 TMA boxes of W rows of tiles I and J. Whole warp.
+template <class C>
+__device__ __forceinline__ void rform_fill(uint8_t *smem, const CUtensorMap *wmap,
+                                           const double *__restrict__ Ek, double Ee, int nlev,
+                                           int kt, bool diag, int ti, int tj) {
+  double *dsm = reinterpret_cast<double *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
+  uint64_t *empty = full + C::STAGES;
+  int *pole_flag = reinterpret_cast<int *>(empty + C::STAGES);
+  const int s = kt % C::STAGES, lane = lane_id();
+  const int k = kt * C::BK + lane;  // BK == 32 == warp size
+  double dv = 0.0;
+  if (k < nlev) {
+    const double diff = __ldg(Ek + k) - Ee;
+    if (fabs(diff) < kPoleGuard) *pole_flag = 1;
+    dv = 1.0 / diff;
+  }
+  dsm[s * C::BK + lane] = dv;
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t bytes = diag ? C::OP_BYTES : 2 * C::OP_BYTES;
+    mbar_arrive_expect_tx(&full[s], bytes);
+    const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+    const int k0 = kt * C::BK;
+    tma_load_2d(base, wmap, &full[s], k0, ti * C::BM);
+    tma_load_2d(base + C::BOX_BYTES, wmap, &full[s], k0 + C::BOXK, ti * C::BM);
+    if (!diag) {
+      tma_load_2d(base + C::OP_BYTES, wmap, &full[s], k0, tj * C::BM);
+      tma_load_2d(base + C::OP_BYTES + C::BOX_BYTES, wmap, &full[s], k0 + C::BOXK, tj * C::BM);
+    }
+  }
+}
+
 // One consumer warp: its chunk's k loop and epilogue (MODE 0: two blocks (r, c), (r, c + 1);
 // MODE 2: one block; MODE 3: no block, only releases the stages). Templated whole so that each
 // mode's accumulators get their own register allocation.
@@ -146,7 +185,8 @@ template <class C, int MODE>
 __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag, int rb0, int cb0,
                                                int ti, int tj, int nch, int64_t e, int pair,
                                                double inv2a, double *__restrict__ R,
-                                               int32_t *__restrict__ status) {
+                                               int32_t *__restrict__ status, const CUtensorMap *wmap,
+                                               const double *__restrict__ Ek, double Ee, int nlev) {
   double *dsm = reinterpret_cast<double *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
   uint64_t *empty = full + C::STAGES;
@@ -179,6 +219,11 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (!C::PRODUCER && warp_id() == kt % C::NCW && kt + C::STAGES < nk) {
+      // this warp's turn: once every warp has released slab kt, refill its slot with kt + STAGES
+      mbar_wait(&empty[s], (kt / C::STAGES) & 1);
+      rform_fill<C>(smem, wmap, Ek, Ee, nlev, kt + C::STAGES, diag, ti, tj);
+    }
   }
 
   // ===================== epilogue: scale, store tile + mirror =====================
@@ -243,7 +288,14 @@ __global__ void __launch_bounds__(C::NT, 1)
   }
   __syncthreads();
 
-  if (warp == C::NCW) {
+  if (!C::PRODUCER) {
+    // prologue: warp 0 fills the first STAGES slabs; afterwards the consumers refill in turn
+    if (warp == 0) {
+      tma_prefetch_desc(&wmap);
+      for (int kt = 0; kt < C::STAGES && kt < nk; ++kt)
+        rform_fill<C>(smem, &wmap, Ek, Ee, nlev, kt, diag, ti, tj);
+    }
+  } else if (warp == C::NCW) {
     // ===================== producer warp: TMA + denominators =====================
     if (lane == 0) tma_prefetch_desc(&wmap);
     int found_pole = 0;
@@ -283,11 +335,14 @@ __global__ void __launch_bounds__(C::NT, 1)
   int rb0, cb0;
   const int nblk = rform_chunk<C::NB, C::NCW>(warp, rbm, cbm, diag, rb0, cb0);
   if (nblk == 2)
-    rform_consumer<C, 0>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status);
+    rform_consumer<C, 0>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status, &wmap,
+                         Ek, Ee, nlev);
   else if (nblk == 1)
-    rform_consumer<C, 2>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status);
+    rform_consumer<C, 2>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status, &wmap,
+                         Ek, Ee, nlev);
   else
-    rform_consumer<C, 3>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status);
+    rform_consumer<C, 3>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status, &wmap,
+                         Ek, Ee, nlev);
 }
 
 // Small-channel path (nch <= 32, e.g. BASELINE.json:7 'tiny'): one CTA per energy, each thread owns
@@ -447,8 +502,11 @@ static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *
   return cudaSuccess;
 }
 
-using Rform128 = RformCfg<128, 3>;
-using Rform64 = RformCfg<64, 3>;
+// Rform128 (dedicated producer warp) and Rform128R (consumers refill in turn, no spills) measure the
+// same on darc (87.5 % vs 87.2 % of peak, profiles/r01_summary.md); RMX_RFORM_PRODUCER=0 selects R.
+using Rform128 = RformCfg<128, 3, true>;
+using Rform128R = RformCfg<128, 3, false>;
+using Rform64 = RformCfg<64, 3, false>;
 
 int rform_tile_for(int64_t nch) {
   if (nch <= 32) return 0;
@@ -474,6 +532,13 @@ cudaError_t launch_rform(const double *w, int64_t ldw, const double *Ek, int64_t
   if (bm == 64)
     return launch_rform_cfg<Rform64>(w, ldw, Ek, static_cast<int>(nch), static_cast<int>(nlev), a,
                                      E, ne, R, status, st, err);
+  static const bool rotating = [] {
+    const char *v = std::getenv("RMX_RFORM_PRODUCER");
+    return v && v[0] == '0';
+  }();
+  if (rotating)
+    return launch_rform_cfg<Rform128R>(w, ldw, Ek, static_cast<int>(nch), static_cast<int>(nlev), a,
+                                       E, ne, R, status, st, err);
   return launch_rform_cfg<Rform128>(w, ldw, Ek, static_cast<int>(nch), static_cast<int>(nlev), a,
                                     E, ne, R, status, st, err);
 }

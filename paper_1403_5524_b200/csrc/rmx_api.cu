@@ -40,8 +40,8 @@ struct rmx_ctx {
     void *p = nullptr;
     size_t bytes = 0;
   } dw, dEk, dE, dF, dG, dFp, dGp, dno, drs, dst;
-  // post-processing scratch (NEXT-4): Gaussian weight table, admixture weights, Maxwell partials
-  Dev dgt, dmix, dpart;
+  // post-processing scratch (NEXT-4): Maxwell partial sums
+  Dev dpart;
   // inner-region eigensolve (NEXT-3): library handles (created on first use) and scratch
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
@@ -231,7 +231,7 @@ rmx_rc rmx_destroy(rmx_ctx *c) {
   cudaFree(c->match_views);
   cudaFree(c->tepi_views);
   for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
-                  &c->dst, &c->dgt, &c->dmix, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg})
+                  &c->dst, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg})
     cudaFree(d->p);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->blas) cublasDestroy(c->blas);
@@ -600,7 +600,8 @@ rmx_rc rmx_convolve_gaussian(rmx_ctx *c, const double *x, int64_t nspec, const d
                              int64_t ne, double dE, double fwhm, double *y) {
   if (!c) return RMX_EINVAL;
   if (!x || !y) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: null pointer");
-  if (nspec < 1 || ne < 1 || nspec > 4096) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: bad sizes");
+  if (nspec < 1 || ne < 1 || nspec > 65535) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: bad sizes");
+  if (mix && nspec > 64) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: at most 64 admixture components");
   if (!(dE > 0.0) || !(fwhm > 0.0)) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: dE, fwhm must be > 0");
   if (fwhm < 2.0 * dE) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: fwhm < 2 dE (under-resolved kernel)");
   const int M = conv_window(dE, fwhm, nullptr);
@@ -615,19 +616,10 @@ rmx_rc rmx_convolve_gaussian(rmx_ctx *c, const double *x, int64_t nspec, const d
   if (mix && !(msum > 0.0)) return fail(c, RMX_EINVAL, "rmx_convolve_gaussian: admixture weights sum to 0");
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
-  rmx_rc rc;
-  if ((rc = grow(c, c->dgt, sizeof(double) * (M + 1))) ||
-      (mix && (rc = grow(c, c->dmix, sizeof(double) * nspec))))
-    return rc;
-  cudaError_t e = cudaSuccess;
-  if (mix) e = cudaMemcpyAsync(c->dmix.p, mix, sizeof(double) * nspec, cudaMemcpyHostToDevice, c->stream);
-  if (e != cudaSuccess) return cuda_fail(c, e, "rmx_convolve_gaussian/mix");
-  e = timed(c, RMX_KID_OTHER, 2, [&] {
-    return launch_convolve(x, nspec, mix ? static_cast<double *>(c->dmix.p) : nullptr, ne, dE, fwhm,
-                           static_cast<double *>(c->dgt.p), y, c->stream);
+  cudaError_t e = timed(c, RMX_KID_OTHER, 1, [&] {
+    return launch_convolve(x, nspec, mix, ne, dE, fwhm, y, c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_convolve_gaussian");
-  if (mix) cudaStreamSynchronize(c->stream);  // mix is a caller host buffer copied asynchronously
   return RMX_OK;
 }
 

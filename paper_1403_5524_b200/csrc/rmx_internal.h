@@ -94,8 +94,8 @@ cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, cons
 // post.cu (NEXT-4); the Gaussian window x[i-M, i+256+M) and its weights live in shared memory
 constexpr int kMaxConvHalfWidth = 9000;
 int conv_window(double dE, double fwhm, double *sigma);
-cudaError_t launch_convolve(const double *x, int64_t nspec, const double *mix_dev, int64_t ne,
-                            double dE, double fwhm, double *gtab, double *y, cudaStream_t st);
+cudaError_t launch_convolve(const double *x, int64_t nspec, const double *mix, int64_t ne,
+                            double dE, double fwhm, double *y, cudaStream_t st);  // mix: HOST, <= 64
 int64_t maxwell_chunks(int64_t ne);
 cudaError_t launch_maxwell(const double *omega, int64_t ne, int64_t npair, const double *E,
                            const double *Eth, const double *kT, int nT, double *part, double *ups,

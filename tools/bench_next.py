@@ -138,17 +138,18 @@ def row_conv(ctx, out):
     ne, dE = 400000, 5e-7
     fwhm = 4e-3 / 13.605693122994  # 4 meV in Ry
     rng = np.random.default_rng(1)
-    x = rng.uniform(0.0, 1.0, (3, ne))
+    nspec = 32  # 32 spectra per call (e.g. Omega(0 -> b) for 32 transitions): the kernel, not the
+    x = rng.uniform(0.0, 1.0, (nspec, ne))  # Python call overhead, dominates the timed region
     xd = torch.from_numpy(x).cuda()
-    ms = timed(lambda: ctx.convolve_gaussian(xd, dE, fwhm, mix=[2.0, 1.0, 1.0]), reps=5, warm=2)
+    ms = timed(lambda: ctx.convolve_gaussian(xd, dE, fwhm), reps=5, warm=2) / nspec
     s = fwhm / (2 * np.sqrt(2 * np.log(2)))
     M = int(np.floor(5 * s / dE))
     flops = 2.0 * (2 * M + 1) * ne  # algorithmic: one multiply-add per window point per output
     instr = (2.0 * M + 1) * ne       # executed FP64 instructions (interior: one DADD + one DFMA per pair)
     t0 = time.perf_counter()
-    oracle.convolve_gaussian(x[:, :4000], dE, fwhm, mix=[2.0, 1.0, 1.0])
+    oracle.convolve_gaussian(x[:1, :4000], dE, fwhm)
     cpu = time.perf_counter() - t0
-    out.append({"row": "NEXT-4 Gaussian convolution + admixture", "workload": f"fine mesh ne={ne}, FWHM 4 meV (M={M}), 3 spectra 2:1:1",
+    out.append({"row": "NEXT-4 Gaussian convolution", "workload": f"fine mesh ne={ne}, FWHM 4 meV (M={M}), 32 spectra per call, ms per spectrum",
                 "ms": ms, "points_per_s": ne / (ms / 1e3), "achieved_tflops": flops / (ms / 1e3) / 1e12,
                 "bound": "alu (FP64 pipe)", "peak": FP64_DFMA_PEAK,
                 "frac_fp64_issue": instr / (ms / 1e3) / (FP64_DFMA_PEAK * 1e12 / 2),
@@ -177,6 +178,7 @@ def row_maxwell(ctx, out):
     out.append({"row": "NEXT-4 Maxwellian average", "workload": "darc mesh ne=100000, 300 pairs, 16 temperatures",
                 "ms": ms, "achieved_gbs": byts / (ms / 1e3) / 1e9, "bound": "hbm", "peak": hbm_peak(),
                 "frac": byts / (ms / 1e3) / 1e9 / hbm_peak(),
+                "note": "Omega [ne][npair] read once; Boltzmann factors shared per (E_i, T) within a chunk",
                 "exp_per_s": ne * 300 * 16 / (ms / 1e3),
                 "cpu_baseline": {"value": 10 / cpu, "unit": "pairs/s", "cores": 1, "kind": "oracle",
                                  "sample": "10 pairs x 16 temperatures"}})
