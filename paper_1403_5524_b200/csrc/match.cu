@@ -25,9 +25,11 @@ struct MatchSmem {
 };
 
 
-// Workspace slot: M [n][ldm] = [A | pad | B_open]; Tg [32][32] (inverse of a diagonal block).
-// After elimination + back substitution the columns [npad, npad + o) of M hold Y = A^{-1} B_open
-// and K[e] = -Y (open columns), -e_j (closed columns).
+// Workspace slot: M [n][ldm] = [A P | pad | B_open] with the unknowns permuted closed-first (P);
+// Tg [32][32] (inverse of a diagonal block). After elimination + back substitution the columns
+// [npad, npad + o) of M hold Y = (A P)^{-1} B_open, and K[e] = -P Y (open columns), -e_j (closed
+// columns); with open_rows_only (the sweep: the T epilogue reads K_oo only) just K_oo is solved for
+// and written.
 // K may alias R (the sweep reuses the R batch buffer): R[e] is fully consumed before K[e] is written.
 // Triangular solves with the 32x32 diagonal blocks run as in-place DMMA GEMMs with their explicit
 // inverses (MAGMA-style); interchanges swap whole augmented rows right of the outer block start.
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(NT, 1)
                  const double *__restrict__ G, const double *__restrict__ Fp,
                  const double *__restrict__ Gp, double a, int n, int64_t ne,
                  const int32_t *__restrict__ n_open, double *K, int64_t ldk, double *ws,
-                 int64_t ws_slot, const CUtensorMap *views, int32_t *status) {
+                 int64_t ws_slot, const CUtensorMap *views, int32_t *status, int open_rows_only) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   MatchSmem &sm = *reinterpret_cast<MatchSmem *>(smem_raw);
   const MatchLayout L = match_layout(n);
@@ -54,6 +56,11 @@ __global__ void __launch_bounds__(NT, 1)
     const int ncols = npad + o;
     const double *Re = R + e * static_cast<int64_t>(n) * ldr;
     const double *Fe = F + e * n, *Ge = G + e * n, *Fpe = Fp + e * n, *Gpe = Gp + e * n;
+    // unknowns ordered closed channels first, open last: column q of A holds channel
+    // jq = (q < nc) ? o + q : q - nc, so the open unknowns are the LAST rows of the triangular
+    // solve and back substitution for K_oo can stop after them (SURVEY §8(a) S4 flops:
+    // (2/3)n^3 + n^2 n_o + n_o^3 instead of (2/3)n^3 + 2 n^2 n_o)
+    const int nc = n - o;
 
     // ---- S3: A_ij = G_i d_ij - a R_ij G'_j ; B_ij = F_i d_ij - a R_ij F'_j (16 loads in flight) ----
     for (int i = warp_id(); i < n; i += NW) {
@@ -68,8 +75,9 @@ __global__ void __launch_bounds__(NT, 1)
           rv[q] = 0.0;
           sv[q] = 0.0;
           if (j < n) {
-            rv[q] = Ri[j];
-            sv[q] = Gpe[j];
+            const int jc = (j < nc) ? o + j : j - nc;
+            rv[q] = Ri[jc];
+            sv[q] = Gpe[jc];
           } else if (j >= npad && j < ncols) {
             rv[q] = Ri[j - npad];
             sv[q] = Fpe[j - npad];
@@ -80,7 +88,7 @@ __global__ void __launch_bounds__(NT, 1)
           const int j = j0 + 32 * q;
           if (j < ncols) {
             double v = -(a * rv[q]) * sv[q];
-            if (j == i) v += Ge[i];
+            if (j < n && ((j < nc) ? o + j : j - nc) == i) v += Ge[i];
             if (j - npad == i) v += Fe[i];
             Mi[j] = v;
           }
@@ -125,23 +133,30 @@ __global__ void __launch_bounds__(NT, 1)
     }
 
     // ---- S4b: blocked back substitution U Y = L^{-1} P B_open (Y = columns [npad, npad+o)) ----
+    // rows_needed: the open unknowns [nc, n) only (sweep), or all (K's closed rows are outputs of
+    // rmx_match_K); the blocks and the update order of rows >= nc are the same either way, so
+    // K_oo is bitwise identical in both modes
+    const int rlo = open_rows_only ? nc : 0;
     if (o > 0) {
-      for (int P0 = ((n - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
+      for (int P0 = ((n - 1) / NB) * NB; P0 >= 0 && P0 + NB > rlo; P0 -= NB) {
         const int W = min(NB, n - P0);
         tri_inv128(Mv, P0, W, TRI_UPPER, Tv, smg, gs);  // U_pp^{-1}
         gemm_set(W, o, W, opk(Tv, 0, 0), opn(Mv, P0, npad), Mv, P0, npad, false, 0.0, smg, gs);
-        if (P0 > 0)
-          gemm_sub(P0, o, W, opk(Mv, 0, P0), opn(Mv, P0, npad), Mv, 0, npad, false, smg, gs);
+        if (P0 > rlo)
+          gemm_sub(P0 - rlo, o, W, opk(Mv, rlo, P0), opn(Mv, P0, npad), Mv, rlo, npad, false, smg, gs);
       }
     }
 
     // ---- output: K = -Y (open columns), -e_j (closed columns); status ----
     int bad = 0;
     double *Ke = K + e * static_cast<int64_t>(n) * ldk;
-    for (int i = warp_id(); i < n; i += NW) {
-      const double *Yi = Mw + static_cast<int64_t>(i) * ldm + npad;
+    const int nrows = open_rows_only ? o : n;
+    const int ncolk = open_rows_only ? o : n;
+    for (int i = warp_id(); i < nrows; i += NW) {
+      const int qi = (i < o) ? nc + i : i - o;  // solution row of channel i
+      const double *Yi = Mw + static_cast<int64_t>(qi) * ldm + npad;
       double *Ki = Ke + static_cast<int64_t>(i) * ldk;
-      for (int j = lane_id(); j < n; j += 32) {
+      for (int j = lane_id(); j < ncolk; j += 32) {
         double v;
         if (j < o) {
           v = -Yi[j];
@@ -173,7 +188,7 @@ void match_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,
                          const double *Gp, double a, int64_t nch, int64_t ne, const int32_t *n_open,
                          double *K, double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
-                         int32_t *status, cudaStream_t st) {
+                         int32_t *status, cudaStream_t st, int open_rows_only) {
   static bool attr = false;
   if (!attr) {
     cudaError_t ce = cudaFuncSetAttribute(match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -183,7 +198,8 @@ cudaError_t launch_match(const double *R, const double *F, const double *G, cons
   }
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
   match_kernel<<<grid, NT, sizeof(MatchSmem), st>>>(R, nch, F, G, Fp, Gp, a, static_cast<int>(nch),
-                                                    ne, n_open, K, nch, ws, ws_slot, views, status);
+                                                    ne, n_open, K, nch, ws, ws_slot, views, status,
+                                                    open_rows_only);
   return cudaGetLastError();
 }
 

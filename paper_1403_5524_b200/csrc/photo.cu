@@ -15,6 +15,7 @@
 // T epilogue (tepi.cu), which already holds the Cholesky factor of I + K_oo^2.
 #include "rmx_common.cuh"
 #include "rmx_internal.h"
+#include <algorithm>
 
 namespace rmx {
 
@@ -26,7 +27,7 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
                                                          const double *__restrict__ Ek,
                                                          const double *__restrict__ d,
                                                          const double *__restrict__ E, int nch,
-                                                         int nlev, int64_t ne,
+                                                         int nlev, int64_t ne, int kchunk,
                                                          double *__restrict__ g,
                                                          int32_t *__restrict__ status) {
   extern __shared__ __align__(16) double dg_smem[];
@@ -42,20 +43,23 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
   for (int r = 0; r < DG_RI; ++r)
 #pragma unroll
     for (int c = 0; c < DG_RE; ++c) acc[r][c] = 0.0;
-  for (int k0 = 0; k0 < nlev; k0 += DG_BK) {
+  // split K: CTA z of gridDim.z sums k in [z kchunk, (z+1) kchunk) into its own partial plane
+  const int kbeg = blockIdx.z * kchunk, kend = min(nlev, kbeg + kchunk);
+  g += static_cast<int64_t>(blockIdx.z) * ne * nch;
+  for (int k0 = kbeg; k0 < kend; k0 += DG_BK) {
     __syncthreads();
     // W slab: 128 channels x 32 k, coalesced 256-byte row segments, stored transposed
     for (int q = threadIdx.x; q < DG_BI * DG_BK; q += DG_NT) {
       const int r = q / DG_BK, kk = q % DG_BK;
       const int i = i0 + r, k = k0 + kk;
-      Wt[kk][r] = (i < nch && k < nlev) ? w[static_cast<int64_t>(i) * ldw + k] : 0.0;
+      Wt[kk][r] = (i < nch && k < kend) ? w[static_cast<int64_t>(i) * ldw + k] : 0.0;
     }
     for (int q = threadIdx.x; q < DG_BK * DG_BE; q += DG_NT) {
       const int kk = q / DG_BE, c = q % DG_BE;
       const int k = k0 + kk;
       const int64_t e = e0 + c;
       double v = 0.0;
-      if (k < nlev && e < ne) {
+      if (k < kend && e < ne) {
         const double diff = Ek[k] - E[e];
         if (fabs(diff) < kPoleGuard) pole[c] = 1;
         v = d[k] / diff;
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
   for (int c = 0; c < DG_RE; ++c) {
     const int64_t e = e0 + tx * DG_RE + c;
     if (e >= ne) continue;
-    const bool pl = pole[tx * DG_RE + c] != 0;
+    const bool pl = pole[tx * DG_RE + c] != 0;  // (per k range; the reduction ORs via NaN)
     if (pl && blockIdx.x == 0 && ty == 0) set_status(status, e, RMX_E_POLE);
 #pragma unroll
     for (int r = 0; r < DG_RI; ++r) {
@@ -92,9 +96,29 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
   }
 }
 
+// g = sum of the nsplit partial planes, in plane order (deterministic)
+__global__ void dipole_g_reduce_kernel(const double *__restrict__ part, int nsplit, int64_t n,
+                                       double *__restrict__ g) {
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < nsplit; ++z) s += part[z * n + q];
+    g[q] = s;
+  }
+}
+
+// K splits so that the grid covers >= 2 CTAs per SM (the energies x channels tile count alone is
+// small for a 296-energy batch: 16 x 5 = 80 CTAs at darc)
+int dipole_g_splits(int64_t nch, int64_t nlev, int64_t ne) {
+  const int64_t tiles = ((nch + DG_BI - 1) / DG_BI) * ((ne + DG_BE - 1) / DG_BE);
+  int64_t s = (2 * 148 + tiles - 1) / tiles;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, nlev / (8 * DG_BK)));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 16)));
+}
+
 cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, const double *d,
                             int64_t nch, int64_t nlev, const double *E, int64_t ne, double *g,
-                            int32_t *status, cudaStream_t st) {
+                            int32_t *status, double *part, int64_t part_cap, cudaStream_t st) {
   constexpr int smem = sizeof(double) * (DG_BK * DG_LDW + DG_BK * DG_BE);
   static bool attr = false;
   if (!attr) {
@@ -105,12 +129,22 @@ cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, cons
   const int64_t max_e = static_cast<int64_t>(65535) * DG_BE;  // grid.y limit
   for (int64_t e0 = 0; e0 < ne; e0 += max_e) {
     const int64_t n = ne - e0 < max_e ? ne - e0 : max_e;
-    dim3 grid(static_cast<unsigned>((nch + DG_BI - 1) / DG_BI), static_cast<unsigned>((n + DG_BE - 1) / DG_BE));
+    int ns = part ? dipole_g_splits(nch, nlev, n) : 1;
+    while (ns > 1 && ns * n * nch > part_cap) --ns;  // never beyond the caller's scratch
+    const int kchunk = static_cast<int>(((nlev + ns - 1) / ns + DG_BK - 1) / DG_BK * DG_BK);
+    dim3 grid(static_cast<unsigned>((nch + DG_BI - 1) / DG_BI), static_cast<unsigned>((n + DG_BE - 1) / DG_BE),
+              static_cast<unsigned>(ns));
     dipole_g_kernel<<<grid, DG_NT, smem, st>>>(w, ldw, Ek, d, E + e0, static_cast<int>(nch),
-                                            static_cast<int>(nlev), n, g + e0 * nch,
+                                            static_cast<int>(nlev), n, kchunk,
+                                            ns > 1 ? part : g + e0 * nch,
                                             status ? status + e0 : nullptr);
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return ce;
+    if (ns > 1) {
+      dipole_g_reduce_kernel<<<592, 256, 0, st>>>(part, ns, n * nch, g + e0 * nch);
+      ce = cudaGetLastError();
+      if (ce != cudaSuccess) return ce;
+    }
   }
   return cudaSuccess;
 }

@@ -46,8 +46,8 @@ struct rmx_ctx {
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   Dev dV, dwork, dinfo;
-  // photoionisation amplitudes g of one sweep batch (NEXT-1)
-  Dev dg;
+  // photoionisation amplitudes g of one sweep batch and the split-K partials (NEXT-1)
+  Dev dg, dgpart;
   // instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> free_events;
@@ -231,7 +231,7 @@ rmx_rc rmx_destroy(rmx_ctx *c) {
   cudaFree(c->match_views);
   cudaFree(c->tepi_views);
   for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
-                  &c->dst, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg})
+                  &c->dst, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg, &c->dgpart})
     cudaFree(d->p);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->blas) cublasDestroy(c->blas);
@@ -395,7 +395,9 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
             static_cast<size_t>(batch) * mat * sizeof(double));
   if (rc != RMX_OK) return rc;
   double *rb = c->rbuf;
-  if (ph && (rc = grow(c, c->dg, sizeof(double) * batch * nch))) return rc;
+  if (ph && ((rc = grow(c, c->dg, sizeof(double) * batch * nch)) ||
+             (rc = grow(c, c->dgpart, sizeof(double) * dipole_g_splits(nch, nlev, batch) * batch * nch))))
+    return rc;
   std::string err;
   for (int64_t b0 = 0; b0 < ne; b0 += batch) {
     const int64_t nb = std::min(batch, ne - b0);
@@ -409,9 +411,15 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
       if (R_d && dump_idx[d] >= b0 && dump_idx[d] < b0 + nb)
         cudaMemcpyAsync(R_d + d * mat, rb + (dump_idx[d] - b0) * mat, mat * sizeof(double),
                         cudaMemcpyDeviceToDevice, c->stream);
+    // the T epilogue reads K_oo only: solve for the open unknowns alone unless this batch dumps a
+    // full K or the photoionisation amplitudes need K's closed rows
+    bool dumps = false;
+    for (int64_t d = 0; d < n_dump; ++d) dumps |= dump_idx[d] >= b0 && dump_idx[d] < b0 + nb;
+    const int open_only = (!dumps && !ph) ? 1 : 0;
     e = timed(c, RMX_KID_MATCH, 1, [&] {
       return launch_match(rb, F + b0 * nch, G + b0 * nch, Fp + b0 * nch, Gp + b0 * nch, a, nch, nb,
-                          nob, rb, c->ws, ws_slot_doubles(nch), c->match_views, slots, stb, c->stream);
+                          nob, rb, c->ws, ws_slot_doubles(nch), c->match_views, slots, stb, c->stream,
+                          open_only);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep/K");
     for (int64_t d = 0; d < n_dump; ++d) {
@@ -435,7 +443,9 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
       // NEXT-1: g for this batch, then the amplitudes inside the T epilogue
       double *gb = static_cast<double *>(c->dg.p);
       e = timed(c, RMX_KID_OTHER, 1, [&] {
-        return launch_dipole_g(w, ldw, Ek, ph->d, nch, nlev, E + b0, nb, gb, stb, c->stream);
+        return launch_dipole_g(w, ldw, Ek, ph->d, nch, nlev, E + b0, nb, gb, stb,
+                               static_cast<double *>(c->dgpart.p),
+                               static_cast<int64_t>(c->dgpart.bytes / sizeof(double)), c->stream);
       });
       if (e != cudaSuccess) return cuda_fail(c, e, "rmx_sweep_photo/g");
       pab.g = gb;
@@ -495,8 +505,13 @@ rmx_rc rmx_dipole_amplitude(rmx_ctx *c, const double *w, int64_t ldw, const doub
   if (ldw < nlev) return fail(c, RMX_EINVAL, "rmx_dipole_amplitude: ldw < nlev");
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
-  cudaError_t e = timed(c, RMX_KID_OTHER, 1, [&] {
-    return launch_dipole_g(w, ldw, Ek, d, nch, nlev, E, ne, g, status, c->stream);
+  const int64_t ne1 = std::min<int64_t>(ne, static_cast<int64_t>(65535) * 64);
+  rmx_rc rc = grow(c, c->dgpart, sizeof(double) * dipole_g_splits(nch, nlev, ne1) * ne1 * nch);
+  if (rc != RMX_OK) return rc;
+  cudaError_t e = timed(c, RMX_KID_OTHER, 2, [&] {
+    return launch_dipole_g(w, ldw, Ek, d, nch, nlev, E, ne, g, status,
+                           static_cast<double *>(c->dgpart.p),
+                           static_cast<int64_t>(c->dgpart.bytes / sizeof(double)), c->stream);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "rmx_dipole_amplitude");
   return RMX_OK;

@@ -59,7 +59,7 @@ void match_view_specs(int64_t nch, std::vector<MatSpec> &specs);
 cudaError_t launch_match(const double *R, const double *F, const double *G, const double *Fp,
                          const double *Gp, double a, int64_t nch, int64_t ne, const int32_t *n_open,
                          double *K, double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
-                         int32_t *status, cudaStream_t st);
+                         int32_t *status, cudaStream_t st, int open_rows_only = 0);
 
 // tepi.cu
 // Optional level-pair output of the T epilogue (NEXT-2): omega [ne][nlevel][nlevel] accumulates
@@ -87,9 +87,12 @@ cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t n
                         const LevelSums &lv, const PhotoArgs &pa, double *ws, int64_t ws_slot,
                         const CUtensorMap *views, int64_t ws_slots, int32_t *status, cudaStream_t st);
 // photo.cu
+// part: scratch of part_cap doubles for the split-K partial planes (splits are reduced to fit;
+// nullptr: no K split)
+int dipole_g_splits(int64_t nch, int64_t nlev, int64_t ne);
 cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, const double *d,
                             int64_t nch, int64_t nlev, const double *E, int64_t ne, double *g,
-                            int32_t *status, cudaStream_t st);
+                            int32_t *status, double *part, int64_t part_cap, cudaStream_t st);
 
 // post.cu (NEXT-4); the Gaussian window x[i-M, i+256+M) and its weights live in shared memory
 constexpr int kMaxConvHalfWidth = 9000;
