@@ -52,6 +52,20 @@ def test_null_ctx_is_einval(lib):
     assert lib.rmx_destroy(None) == 1
     assert lib.rmx_build_R(None, None, 0, None, 0, 0, 1.0, None, 0, None, None) == 1
     assert lib.rmx_last_error(None) == b"null ctx"
+    # every other entry point rejects a null context synchronously, before touching CUDA
+    assert lib.rmx_match_K(None, None, None, None, None, None, 1.0, 1, 1, None, None, None) == 1
+    assert lib.rmx_collision_strength(None, None, 1, 1, None, None, None, None) == 1
+    assert lib.rmx_collision_strength_levels(None, None, 1, 1, None, None, 1, 1.0, None, None) == 1
+    assert lib.rmx_sweep_levels(None, None, 2, None, 1, 1, 1.0, None, 1, None, None, None, None, None, 0,
+                                None, 1, 1.0, None, None, None) == 1
+    assert lib.rmx_dipole_amplitude(None, None, 2, None, None, 1, 1, None, 1, None, None) == 1
+    assert lib.rmx_photoionization(None, None, None, None, None, None, 1, 1, None, 0.0, 1.0, None, None,
+                                   None) == 1
+    assert lib.rmx_sweep_photo(None, None, 2, None, None, 1, 1, 1.0, None, 1, None, None, None, None,
+                               None, 0, 0.0, 1.0, None, None, None) == 1
+    assert lib.rmx_inner_region(None, None, 1, None, 1, None, None, 1) == 1
+    assert lib.rmx_convolve_gaussian(None, None, 1, None, 1, 1.0, 3.0, None) == 1
+    assert lib.rmx_maxwell_average(None, None, 1, 1, None, None, None, 1, None) == 1
 
 
 @pytest.mark.skipif(shutil.which("cuobjdump") is None and not os.path.exists("/usr/local/cuda/bin/cuobjdump"),
