@@ -39,7 +39,14 @@ FP64_DMMA_PEAK_TFLOPS = 37.1
 FP64_DFMA_PEAK_TFLOPS = 34.2
 
 
-def ncu_traffic(workload: str, batch: int):
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic(workload: str, batch: int, kernel: str = "rform"):
     """DRAM bytes (read + write) per launch of the R kernel from the newest committed full ncu
     capture (profiles/rNN_ncu_kernels.json, written by tools/summarize_profiles.py), when that
     capture was taken on the same workload and energies per launch; else None."""
@@ -50,7 +57,7 @@ def ncu_traffic(workload: str, batch: int):
         except (OSError, ValueError):
             continue
         for name, ent in d.items():
-            if "rform" not in name:
+            if kernel not in name:
                 continue
             wl = ent.get("workload", {})
             rd, wr = ent.get("dram__bytes_read.bytes"), ent.get("dram__bytes_write.bytes")
@@ -70,6 +77,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--oracle-sample", type=int, default=1, help="energies in the oracle sample")
+    p.add_argument("--r-algo", default="int8", choices=["dmma", "int8"],
+                   help="R formation: exact CRT on the INT8 tensor cores (default, rint8.cu) or the FP64 DMMA "
+                        "contraction (rform.cu)")
     return p.parse_args()
 
 
@@ -203,6 +213,8 @@ def main():
         if case is None:
             case = syn.make_case(args.config)  # thresholds + mesh (W/Ek above come from the broadcast)
     ctx = rmx.Context(local)
+    if args.r_algo == "int8":
+        ctx.set_r_algo(rmx.R_INT8)
     ne = case.ne
     batch = args.batch if args.batch > 0 else 2 * torch.cuda.get_device_properties(dev).multi_processor_count
     if args.config in ("tiny", "small") and args.batch <= 0:
@@ -276,6 +288,7 @@ def main():
         ft += float(np.sum(c))
     achieved_r = fr / (ms_r / 1e3) / 1e12 if ms_r > 0 else None
     path_tflops = (fr + fk + ft) / (ms / 1e3) / 1e12
+    ms_g, n_g = stats.get("i8gemm", (0.0, 0))
 
     # ---- results gather (one all-gather, outside the timed region) ---------------------------
     gather_ms = None
@@ -354,27 +367,53 @@ def main():
                          f"{dt:.1f} s, OpenMP over rows/energies"}
 
     if rank == 0:
-        traffic, traffic_src = ncu_traffic(args.config, batch)
+        if args.r_algo == "int8":
+            # dominant kernel: the INT8 tensor-core GEMMs of the CRT R formation. Algorithmic int8 ops per
+            # energy: 16 moduli x nch(nch+1) nlev (upper triangle, like the fp64 count). Peak: the INT8 dense
+            # rate = measured bf16 (sustained: the GEMMs run inside a long step) x the nominal int8/bf16 ratio 2.
+            pk = measured_peaks()
+            peak_i8 = 2.0 * float(pk.get("bf16_tflops_sustained", 1378.4))
+            ops_i8 = 16.0 * fr
+            ach_i8 = ops_i8 / (ms_g / 1e3) / 1e12 if ms_g > 0 else None
+            traffic, traffic_src = ncu_traffic(args.config, batch, kernel="oz_gemm")
+            roofline = {"bound": "tensor", "kernel": "oz_gemm_kernel (INT8 tcgen05, 16 moduli, CRT R formation)",
+                        "achieved": ach_i8, "peak": peak_i8, "unit": "TOPS",
+                        "frac": (ach_i8 / peak_i8) if ach_i8 else None,
+                        "traffic": traffic, "traffic_source": traffic_src,
+                        "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (nominal int8/bf16 ratio, "
+                                       "B200_PROFILING.md); nominal dense int8 4500 TOPS",
+                        "algorithmic": "16 x nch(nch+1) x nlev int8 ops per energy x energies per launch"}
+            r_form = {"algo": "int8-crt (rint8.cu)", "fp64_equivalent_tflops": achieved_r,
+                      "vs_fp64_dmma_peak": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,
+                      "i8gemm_ms": round(ms_g, 3), "rform_total_ms": round(ms_r, 3)}
+        else:
+            traffic, traffic_src = ncu_traffic(args.config, batch)
+            roofline = {"bound": "tensor", "kernel": "rform (FP64 DMMA R formation)",
+                        "achieved": achieved_r, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,
+                        "traffic": traffic, "traffic_source": traffic_src,
+                        "peak_source": "measured FP64 DMMA.8x8x4 peak, tools/fp64_peak.cu on this pool "
+                                       "(profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry",
+                        "algorithmic": "nch(nch+1)*nlev flops per energy x energies per launch"}
+            r_form = {"algo": "fp64-dmma (rform.cu)"}
         line = {
             "metric": "energies/sec (R->K->|T|^2 sweep)",
             "value": value, "unit": "energies/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (rmx_synth, seed 0)",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.r_algo == "dmma" else "f64 (R: exact int8 CRT on tcgen05; K, T: f64 DMMA)",
+            "data": "synthetic (rmx_synth, seed 0)",
             "config": {"workload": args.config, "nch": nch, "nlev": nlev, "ne_mesh": ne,
                        "a": cfg["a"], "energies_per_step_per_gpu": batch,
                        "parallelism": f"energy-sharded block-cyclic x{world}",
                        "l2": f"inputs exceed L2 (W = {nch * nlev * 8 / 1e6:.0f} MB, 126 MB L2)"
                        if nch * nlev * 8 > 126e6 else "W fits L2; R/K batch buffers exceed L2"},
-            "roofline": {"bound": "tensor", "kernel": "rform (FP64 DMMA R formation)",
-                         "achieved": achieved_r, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,
-                         "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_source": "measured FP64 DMMA.8x8x4 peak, tools/fp64_peak.cu on this pool "
-                                        "(profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry",
-                         "algorithmic": "nch(nch+1)*nlev flops per energy x energies per launch"},
+            "roofline": roofline,
+            "r_formation": r_form,
             "kernel_ms": {k: round(v[0], 3) for k, v in stats.items() if k != "launches"},
             "path_fp64_tflops": path_tflops,
-            "path_fp64_frac": path_tflops / FP64_DMMA_PEAK_TFLOPS,
+            ("path_fp64_frac" if args.r_algo == "dmma" else "path_fp64_equivalent_vs_dmma_peak"):
+                path_tflops / FP64_DMMA_PEAK_TFLOPS,
             "gpu_launches": int(stats["launches"]),
             "bad_status_energies": bad,
             "clocks": clk.summary(),

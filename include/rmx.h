@@ -299,13 +299,28 @@ rmx_rc rmx_maxwell_average(rmx_ctx *ctx, const double *omega, int64_t ne, int64_
  * DEVICE int32 status[ne] (pass status=NULL to skip). Returns sticky CUDA errors. */
 rmx_rc rmx_sync(rmx_ctx *ctx, const int32_t *status, int64_t ne, int64_t *n_bad);
 
+/*
+ * rmx_set_r_algo - choose how rmx_build_R / rmx_sweep* form R on this context:
+ *   RMX_R_DMMA (default): the FP64 tensor-core (DMMA) contraction of rform.cu;
+ *   RMX_R_INT8: the same R by exact integer arithmetic on the INT8 tensor cores (tcgen05 kind::i8):
+ *     X = W diag(d) and W rounded to 55 / 53-bit fixed point per row, 16 modular INT8 GEMMs, CRT
+ *     reconstruction (rint8.cu); R error at the level of an fp64 contraction
+ *     (normwise ~1e-14). Needs nlev <= 131071 (int32 accumulator bound), else DMMA is used.
+ *     Workspace ~ 8 x 16 x nch x nlev bytes.
+ */
+enum { RMX_R_DMMA = 0, RMX_R_INT8 = 1 };
+rmx_rc rmx_set_r_algo(rmx_ctx *ctx, int algo);
+
 /* ---- instrumentation (bench / roofline evidence; not needed for correctness) ----------
  * When enabled, every kernel launch is bracketed by cudaEvents on the ctx stream and its
  * duration accumulated per kernel id: 0 = R formation, 1 = matching, 2 = T epilogue,
- * 3 = other (pole scan, packing). rmx_stats reads (total ms, launch count) per id and the
+ * 3 = other (post-processing, dipole amplitudes, eigensolve), 4 = the INT8 GEMM launches of the
+ * RMX_R_INT8 R formation (a subset of 0's time). rmx_stats reads (total ms, launch count) per id and the
  * total number of kernel launches since the last reset (counted whether or not timing is
  * enabled). */
-enum { RMX_KID_RFORM = 0, RMX_KID_MATCH = 1, RMX_KID_TEPI = 2, RMX_KID_OTHER = 3, RMX_NKID = 4 };
+enum { RMX_KID_RFORM = 0, RMX_KID_MATCH = 1, RMX_KID_TEPI = 2, RMX_KID_OTHER = 3,
+       RMX_KID_I8GEMM = 4 /* the INT8 tensor-core GEMMs inside R formation (RMX_R_INT8), also in RFORM */,
+       RMX_NKID = 5 };
 rmx_rc rmx_set_timing(rmx_ctx *ctx, int enable);
 rmx_rc rmx_reset_stats(rmx_ctx *ctx);
 rmx_rc rmx_stats(rmx_ctx *ctx, double *ms_per_kid /* [RMX_NKID] */,

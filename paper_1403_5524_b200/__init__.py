@@ -26,8 +26,10 @@ LIB_PATH = os.path.join(_PKG, "librmx.so")
 
 RMX_OK, RMX_EINVAL, RMX_ENOMEM, RMX_ECUDA = 0, 1, 2, 3
 E_OK, E_POLE, E_SINGULAR, E_NONFINITE = 0, 1, 2, 3
-KID_RFORM, KID_MATCH, KID_TEPI, KID_OTHER = 0, 1, 2, 3
-KID_NAMES = ("rform", "match", "tepi", "other")
+KID_RFORM, KID_MATCH, KID_TEPI, KID_OTHER, KID_I8GEMM = 0, 1, 2, 3, 4
+KID_NAMES = ("rform", "match", "tepi", "other", "i8gemm")
+NKID = len(KID_NAMES)
+R_DMMA, R_INT8 = 0, 1
 
 # every symbol include/rmx.h declares (tests/test_abi.py checks the header and the .so agree)
 EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rmx_build_R",
@@ -36,7 +38,8 @@ EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rm
             "rmx_sweep_photo", "rmx_inner_region", "rmx_convolve_gaussian",
             "rmx_maxwell_average",
             "rmx_sync",
-            "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version", "rmx_sm_target")
+            "rmx_set_r_algo", "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version",
+            "rmx_sm_target")
 
 
 class RmxError(RuntimeError):
@@ -76,6 +79,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "rmx_maxwell_average": [P, P, i64, i64, P, P, P, i64, P],
         "rmx_sync": [P, P, i64, P],
         "rmx_set_timing": [P, i32],
+        "rmx_set_r_algo": [P, i32],
         "rmx_reset_stats": [P],
         "rmx_stats": [P, P, P, P],
     }
@@ -418,6 +422,10 @@ class Context:
         return ups
 
     # ------------------------------------------------------------------ instrumentation
+    def set_r_algo(self, algo: int):
+        """rmx_set_r_algo: R_DMMA (FP64 tensor cores, default) or R_INT8 (exact CRT on INT8 tensor cores)."""
+        self._check(self.lib.rmx_set_r_algo(self._h, int(algo)), "rmx_set_r_algo")
+
     def set_timing(self, on: bool = True):
         self._check(self.lib.rmx_set_timing(self._h, 1 if on else 0), "rmx_set_timing")
 
@@ -425,11 +433,11 @@ class Context:
         self._check(self.lib.rmx_reset_stats(self._h), "rmx_reset_stats")
 
     def stats(self):
-        ms = (ctypes.c_double * 4)()
-        cnt = (ctypes.c_int64 * 4)()
+        ms = (ctypes.c_double * NKID)()
+        cnt = (ctypes.c_int64 * NKID)()
         tot = ctypes.c_int64()
         self._check(self.lib.rmx_stats(self._h, ms, cnt, ctypes.byref(tot)), "rmx_stats")
-        return {KID_NAMES[k]: (ms[k], cnt[k]) for k in range(4)} | {"launches": tot.value}
+        return {KID_NAMES[k]: (ms[k], cnt[k]) for k in range(NKID)} | {"launches": tot.value}
 
     def sync(self, status=None):
         n_bad = ctypes.c_int64()

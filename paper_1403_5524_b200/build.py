@@ -13,7 +13,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librmx.so")
-SOURCES = ["rform.cu", "match.cu", "tepi.cu", "photo.cu", "post.cu", "rmx_api.cu"]
+SOURCES = ["rform.cu", "rint8.cu", "match.cu", "tepi.cu", "photo.cu", "post.cu", "rmx_api.cu"]
 HEADERS = ["rmx_common.cuh", "cta_la.cuh", "rmx_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

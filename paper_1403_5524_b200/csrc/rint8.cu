@@ -1,0 +1,582 @@
+// rint8.cu - R formation on the INT8 tensor cores (tcgen05.mma kind::i8) with exact FP64-level
+// accuracy, by the Chinese-remainder (Ozaki-II-style) emulation of the fp64 contraction
+//     R_ij(E) = (1/2a) sum_k w_ik w_jk / (E_k - E)          (Eq. 1-2; BASELINE.json:5)
+// (readings Z1-Z3). Same C-ABI semantics as rform.cu; selected per context.
+//
+//   1. d_k(E) = 1/(E_k - E) and dmax(E) = max_k |d_k| (pole guard as everywhere: |E - E_k| < 1e-10).
+//   2. Fixed-point operands (exact integers):  X'_ik = rint(w_ik d_k 2^{s_i}),  |X'| <= 2^54, with
+//      s_i from the bound max_k|w_ik| dmax;  W'_jk = rint(w_jk 2^{t_j}),  |W'| <= 2^52.
+//      Then P_ij = sum_k X'_ik W'_jk is an exact integer, |P| <= nlev 2^106 < M/2 for nlev < 2^17,
+//      M = prod of the 16 pairwise-coprime moduli below (2^125.19).
+//   3. For each modulus m_l: V_l = X' mod m_l, U_l = W' mod m_l as signed int8 (|.| <= 128); the INT8
+//      tensor-core GEMM C_l = V_l U_l^T is exact in int32 (|C| <= 128^2 nlev < 2^31), its residue
+//      C_l mod m_l = P mod m_l.
+//   4. CRT (direct formula, exact 128-bit wrapping arithmetic) recovers P_ij in (-M/2, M/2); then
+//      R_ij = P_ij 2^{-s_i - t_j} / (2a), upper triangle mirrored (bitwise symmetric R).
+// The only approximation is the rounding of X and W to 55 / 53 significant bits relative to the row
+// bound (step 2): measured normwise error 3e-14 on darc rows (tools/ozaki_error.py), the level of an
+// fp64 contraction; everything after it is exact integer arithmetic.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "rmx_common.cuh"
+#include "rmx_internal.h"
+
+namespace rmx {
+namespace i8 {
+
+constexpr int L = 16;
+__host__ __device__ constexpr int mod_of(int l) {
+  constexpr int m[L] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191};
+  return m[l];
+}
+constexpr int BX = 54, BW = 52;  // fixed-point magnitudes 2^BX, 2^BW
+
+// ---------------------------------------------------------------------------------------------
+// residues of a 55-bit signed integer u - 2^54 (u = X' + 2^54 in [0, 2^55]) for all 16 moduli,
+// as balanced int8 (r > 127 -> r - m)
+__device__ __forceinline__ int8_t bal(int r, int m) { return static_cast<int8_t>(r > 127 ? r - m : r); }
+
+struct ModConst {
+  int c36, c18, off;  // 2^36 mod m, 2^18 mod m, (m * 2^10 - (2^BIAS mod m)) so that s stays >= 0
+  float inv;          // 1/m (rounded down a little: q never overestimates by more than 1)
+  uint32_t magic;     // ceil(2^32 / m): umulhi(s, magic) is floor(s/m) or one more for s < 2^28
+};
+__constant__ ModConst c_mod[L];
+
+// s mod m for s < 2^28 by multiply-high: 3 integer ops + 1 correction
+__device__ __forceinline__ int umod_magic(uint32_t s, int m, uint32_t magic) {
+  int r = static_cast<int>(s) - static_cast<int>(__umulhi(s, magic)) * m;
+  return r + ((r < 0) ? m : 0);
+}
+
+__device__ __forceinline__ int umod_small(uint32_t s, int m, float inv) {
+  int q = static_cast<int>(__uint2float_rz(s) * inv);
+  int r = static_cast<int>(s) - q * m;
+  r += (r < 0) ? m : 0;
+  r -= (r >= m) ? m : 0;
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// per energy: d_k = 1/(E_k - E) into dbuf [ne][nlev], dmax [ne], pole flags (status)
+__global__ void __launch_bounds__(256) oz_denom_kernel(const double *__restrict__ Ek, const double *__restrict__ E,
+                                                       int nlev, double *__restrict__ dbuf,
+                                                       double *__restrict__ dmax, int32_t *__restrict__ pflag,
+                                                       int32_t *__restrict__ status) {
+  const int64_t e = blockIdx.x;
+  const double Ee = E[e];
+  double mx = 0.0;
+  int pole = 0;
+  for (int k = threadIdx.x; k < nlev; k += blockDim.x) {
+    const double diff = Ek[k] - Ee;
+    if (fabs(diff) < kPoleGuard) pole = 1;
+    const double d = 1.0 / diff;
+    dbuf[e * nlev + k] = d;
+    mx = fmax(mx, fabs(d));
+  }
+  __shared__ double red[8];
+  __shared__ int pr[8];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    pole |= __shfl_xor_sync(0xffffffffu, pole, off);
+  }
+  if (lane_id() == 0) {
+    red[warp_id()] = mx;
+    pr[warp_id()] = pole;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    int p = 0;
+    for (int q = 0; q < 8; ++q) {
+      m = fmax(m, red[q]);
+      p |= pr[q];
+    }
+    dmax[e] = m;
+    pflag[e] = p;
+    if (p) set_status(status, e, RMX_E_POLE);
+  }
+}
+
+// row maxima of |w| (once per call)
+__global__ void __launch_bounds__(256) oz_rowmax_kernel(const double *__restrict__ w, int64_t ldw, int nlev,
+                                                        double *__restrict__ rowmax) {
+  const int64_t i = blockIdx.x;
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < nlev; k += blockDim.x) mx = fmax(mx, fabs(w[i * ldw + k]));
+  __shared__ double red[8];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane_id() == 0) red[warp_id()] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int q = 0; q < 8; ++q) m = fmax(m, red[q]);
+    rowmax[i] = m;
+  }
+}
+
+// Fixed-point conversion + residues. One CTA per (row i, 2048-wide k chunk); each thread 8
+// consecutive k, its 8 w values loaded once and reused for all ne energies of the chunk.
+// dbuf == nullptr: the W operand (d = 1, BW bits, ne = 1); else the X operands of energies 0..ne-1.
+// out: planes [ne][L][nch][ldv] int8 (ldv multiple of 16); shift: [ne][nch] exponents s_i / t_j.
+__global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restrict__ w, int64_t ldw, int nch,
+                                                         int nlev, int ne, const double *__restrict__ dbuf,
+                                                         const double *__restrict__ dmax,
+                                                         const double *__restrict__ rowmax, int bits,
+                                                         int64_t ldv, int8_t *__restrict__ out,
+                                                         int32_t *__restrict__ shift) {
+  const int i = blockIdx.y;
+  const int k0 = (blockIdx.x * 256 + threadIdx.x) * 8;
+  double wv[8];
+  const double *wr = w + static_cast<int64_t>(i) * ldw + k0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) wv[q] = (k0 + q < nlev) ? wr[q] : 0.0;
+  const int64_t plane = static_cast<int64_t>(nch) * ldv;
+  const uint64_t bias = static_cast<uint64_t>(1) << BX;
+  for (int e = 0; e < ne; ++e) {
+    // scale 2^s with bound * 2^s < 2^bits (bound = max|w_i.| * max|d|): frexp(bound) = f 2^ex, f < 1
+    const double bound = rowmax[i] * (dbuf ? dmax[e] : 1.0);
+    int ex = 0;
+    if (bound > 0.0 && isfinite(bound)) frexp(bound, &ex);
+    const int s = bits - ex;
+    const double scale = ldexp(1.0, s);  // exact power of two
+    if (blockIdx.x == 0 && threadIdx.x == 0) shift[static_cast<int64_t>(e) * nch + i] = s;
+    if (k0 >= nlev) continue;
+    const double *dr = dbuf ? dbuf + static_cast<int64_t>(e) * nlev + k0 : nullptr;
+    uint32_t u2[8], u1[8], u0[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      double x = wv[q];
+      if (dr && k0 + q < nlev) x *= dr[q];
+      x *= scale;
+      if (!isfinite(x)) x = 0.0;  // pole energies: R is NaN anyway (status POLE)
+      const uint64_t u = static_cast<uint64_t>(__double2ll_rn(x) + static_cast<long long>(bias));
+      u2[q] = static_cast<uint32_t>(u >> 36);
+      u1[q] = static_cast<uint32_t>((u >> 18) & 0x3FFFF);
+      u0[q] = static_cast<uint32_t>(u & 0x3FFFF);
+    }
+    int8_t *o = out + static_cast<int64_t>(e) * L * plane + static_cast<int64_t>(i) * ldv + k0;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const int m = mod_of(l);
+      const ModConst mc = c_mod[l];
+      uint32_t pk[2] = {0u, 0u};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t sv = u2[q] * mc.c36 + u1[q] * mc.c18 + u0[q] + mc.off;
+        const int r = umod_magic(sv, m, mc.magic);
+        pk[q >> 2] |= (static_cast<uint32_t>(static_cast<uint8_t>(bal(r, m))) << (8 * (q & 3)));
+      }
+      *reinterpret_cast<uint2 *>(o + l * plane) = make_uint2(pk[0], pk[1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// tcgen05 INT8 GEMM over (upper-triangle tile, modulus, energy):
+//   C = V[e][l] (128 rows of X residues) . U[l]^T (256 rows of W residues), int32 in TMEM,
+//   epilogue: C mod m_l -> uint8 residue plane res[e][l][i][j] (row pitch ldr bytes)
+constexpr int BM = 128, BN = 256, BKB = 128, STAGES = 4;
+constexpr int A_BYTES = BM * BKB, B_BYTES = BN * BKB, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int GEMM_NT = 256;
+constexpr int GEMM_SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                           (static_cast<uint32_t>(BM >> 4) << 24);
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;           // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;   // SBO: 8-row groups 1024 B apart
+  d |= static_cast<uint64_t>(1) << 46;           // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;           // SWIZZLE_128B
+  return d;
+}
+
+__global__ void __launch_bounds__(GEMM_NT, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu, int nch,
+                   int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *accf = empty + STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
+  const int warp = warp_id(), lane = lane_id();
+  const int tile = blockIdx.x % ntiles;
+  const int l = (blockIdx.x / ntiles) % L;
+  const int64_t e = blockIdx.x / (ntiles * L);
+  const int2 tij = tiles[tile];  // (I, J): rows I*128.., columns J*256..
+  const int nk = (nlev + BKB - 1) / BKB;
+  const int vrow = static_cast<int>((e * L + l) * nch) + tij.x * BM;  // row in the stacked V planes
+  const int urow = l * nch + tij.y * BN;                                // row in the stacked U planes
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tv);
+    tma_prefetch_desc(&tu);
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % STAGES;
+      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+      mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+      const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+      tma_load_2d(base, &tv, &full[s], kt * BKB, vrow);
+      tma_load_2d(base + A_BYTES, &tu, &full[s], kt * BKB, urow);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % STAGES;
+      mbar_wait(&full[s], (kt / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+      const uint64_t da = umma_desc_sw128(base), db = umma_desc_sw128(base + A_BYTES);
+#pragma unroll
+      for (int k = 0; k < BKB / 32; ++k) {
+        const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(IDESC), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(&empty[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(accf))
+                 : "memory");
+  } else if (warp >= 4) {
+    // epilogue: TMEM lane quarter q = warp - 4 holds rows q*32 .. q*32+31 of the tile
+    mbar_wait(accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const int q = warp - 4;
+    const int row = tij.x * BM + q * 32 + lane;
+    const int m = mod_of(l);
+    const int c16 = (1 << 16) % m;
+    const float inv = c_mod[l].inv;
+    uint8_t *rrow = res + ((e * L + l) * static_cast<int64_t>(nch) + row) * ldr + tij.y * BN;
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+            "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+            "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+      const int col0 = tij.y * BN + c0;
+      if (row < nch && col0 < nch) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          // acc = h 2^16 + lo (h signed): residue of h c16 + lo (|.| < 2^24: exact in fp32)
+          const int acc = static_cast<int>(v[j]);
+          const int h = acc >> 16, lo = acc & 0xFFFF;
+          const int sv = h * c16 + lo + (m << 16);  // > 0 (|h c16| < 2^15 * 255)
+          const int r = umod_small(static_cast<uint32_t>(sv), m, inv);
+          if ((j & 3) == 0) pk[j >> 2] = 0u;
+          pk[j >> 2] |= static_cast<uint32_t>(r) << (8 * (j & 3));
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(rrow + c0);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
+}
+
+// ---------------------------------------------------------------------------------------------
+// CRT: residues r_l of P_ij -> P_ij -> R_ij. Direct formula: with C_l = (M/m_l)((M/m_l)^-1 mod m_l),
+// S = sum_l r_l C_l = P (mod M), and S/M = sum_l r_l f_l with f_l = C_l/M = inv_l/m_l in (0, 1); since
+// |P| < 2^121.3 < M/16, q = rint(sum_l r_l f_l) (fp64 error < 1e-11) is exactly the multiple of M to
+// remove, and P = S - q M is evaluated exactly in 128-bit wrapping arithmetic (4 x 32-bit limbs).
+struct CrtConst {
+  uint32_t C[L][4];  // C_l, little-endian limbs
+  double f[L];       // inv_l / m_l
+  uint32_t M[4];     // product of the moduli
+};
+__constant__ CrtConst c_crt;
+
+__global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t *__restrict__ res, int64_t ldr, int nch,
+                                                     const int32_t *__restrict__ sx, const int32_t *__restrict__ tw,
+                                                     double inv2a, const int32_t *__restrict__ pflag,
+                                                     double *__restrict__ R) {
+  // rows i and nch-1-i share a block row (upper triangle: nch+1 entries per pair of rows)
+  const int64_t e = blockIdx.z;
+  const int pr = blockIdx.y;  // row pair
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int len0 = nch - pr;  // entries j >= i of row pr
+  int i, j;
+  if (t < len0) {
+    i = pr;
+    j = pr + t;
+  } else {
+    i = nch - 1 - pr;
+    j = i + (t - len0);
+    if (i <= pr || j >= nch) return;
+  }
+  double *Re = R + e * static_cast<int64_t>(nch) * nch;
+  if (pflag[e]) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    Re[static_cast<int64_t>(i) * nch + j] = nan;
+    Re[static_cast<int64_t>(j) * nch + i] = nan;
+    return;
+  }
+  const int64_t plane = static_cast<int64_t>(nch) * ldr;
+  const uint8_t *rp = res + e * L * plane + static_cast<int64_t>(i) * ldr + j;
+  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  double sf = 0.0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const uint32_t r = rp[l * plane];
+    a0 += static_cast<uint64_t>(r) * c_crt.C[l][0];
+    a1 += static_cast<uint64_t>(r) * c_crt.C[l][1];
+    a2 += static_cast<uint64_t>(r) * c_crt.C[l][2];
+    a3 += static_cast<uint64_t>(r) * c_crt.C[l][3];
+    sf = fma(static_cast<double>(r), c_crt.f[l], sf);
+  }
+  // S mod 2^128 from the limb sums (each < 2^44)
+  a1 += a0 >> 32;
+  a2 += a1 >> 32;
+  a3 += a2 >> 32;
+  uint64_t lo = (a0 & 0xFFFFFFFFull) | (a1 << 32);
+  uint64_t hi = (a2 & 0xFFFFFFFFull) | (a3 << 32);
+  // - q M
+  const uint64_t q = static_cast<uint64_t>(rint(sf));
+  const uint64_t m01 = (static_cast<uint64_t>(c_crt.M[1]) << 32) | c_crt.M[0];
+  const uint64_t m23 = (static_cast<uint64_t>(c_crt.M[3]) << 32) | c_crt.M[2];
+  const uint64_t qlo = q * m01, qhi = __umul64hi(q, m01) + q * m23;
+  const uint64_t nlo = lo - qlo;
+  hi = hi - qhi - (lo < qlo ? 1ull : 0ull);
+  lo = nlo;
+  const bool neg = static_cast<int64_t>(hi) < 0;
+  if (neg) {  // negate the 128-bit two's complement value
+    lo = ~lo + 1;
+    hi = ~hi + (lo == 0 ? 1ull : 0ull);
+  }
+  double p = static_cast<double>(hi) * 18446744073709551616.0 + static_cast<double>(lo);
+  if (neg) p = -p;
+  const double r = ldexp(p, -(sx[e * nch + i] + tw[j])) * inv2a;
+  Re[static_cast<int64_t>(i) * nch + j] = r;
+  Re[static_cast<int64_t>(j) * nch + i] = r;
+}
+
+}  // namespace i8
+
+// ---------------------------------------------------------------------------------------------
+// host side
+static bool g_i8_consts = false;
+
+static cudaError_t init_i8_consts() {
+  if (g_i8_consts) return cudaSuccess;
+  i8::ModConst mc[i8::L];
+  i8::CrtConst cc{};
+  unsigned __int128 M = 1;
+  for (int l = 0; l < i8::L; ++l) M *= static_cast<unsigned>(i8::mod_of(l));
+  for (int l = 0; l < i8::L; ++l) {
+    const int m = i8::mod_of(l);
+    const uint64_t p54 = (static_cast<uint64_t>(1) << i8::BX) % m;
+    mc[l].c36 = static_cast<int>((static_cast<uint64_t>(1) << 36) % m);
+    mc[l].c18 = static_cast<int>((static_cast<uint64_t>(1) << 18) % m);
+    mc[l].off = static_cast<int>(m * 1024 - static_cast<int>(p54));
+    mc[l].inv = nextafterf(1.0f / static_cast<float>(m), 0.0f);
+    mc[l].magic = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 32) + m - 1) / m);
+    // C_l = (M/m) * ((M/m)^-1 mod m)
+    const unsigned __int128 Ml = M / static_cast<unsigned>(m);
+    const int Mlm = static_cast<int>(Ml % static_cast<unsigned>(m));
+    int inv = 0;
+    for (int x = 1; x < m; ++x)
+      if ((Mlm * x) % m == 1) { inv = x; break; }
+    const unsigned __int128 C = Ml * static_cast<unsigned>(inv);
+    for (int k = 0; k < 4; ++k) cc.C[l][k] = static_cast<uint32_t>(C >> (32 * k));
+    cc.f[l] = static_cast<double>(inv) / static_cast<double>(m);
+  }
+  for (int k = 0; k < 4; ++k) cc.M[k] = static_cast<uint32_t>(M >> (32 * k));
+  cudaError_t e = cudaMemcpyToSymbol(i8::c_mod, mc, sizeof(mc));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(i8::c_crt, &cc, sizeof(cc));
+  if (e == cudaSuccess) g_i8_consts = true;
+  return e;
+}
+
+static bool encode_i8(CUtensorMap *map, const void *base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                      std::string &err) {
+  typedef CUresult (*Enc)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                          const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                          CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Enc enc = nullptr;
+  if (!enc) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      err = "cuTensorMapEncodeTiled unavailable";
+      return false;
+    }
+    enc = reinterpret_cast<Enc>(p);
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(i8::BKB), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled (int8) failed (code " + std::to_string(static_cast<int>(r)) + ")";
+    return false;
+  }
+  return true;
+}
+
+int64_t rint8_ldv(int64_t nlev) { return (nlev + 15) & ~static_cast<int64_t>(15); }
+int64_t rint8_ldr(int64_t nch) { return (nch + 255) & ~static_cast<int64_t>(255); }
+int rint8_max_nlev() { return 131071; }
+
+// Workspace (bytes) for chunks of ne energies, double-buffered (V planes, d, dmax, shifts, pole flags)
+// plus the W residues, one residue-plane buffer and the tile list
+size_t rint8_ws_bytes(int64_t nch, int64_t nlev, int64_t ne) {
+  const int64_t ldv = rint8_ldv(nlev), ldr = rint8_ldr(nch);
+  size_t b = 0;
+  b += static_cast<size_t>(i8::L) * nch * ldv;                       // U planes
+  b += 2 * static_cast<size_t>(ne) * i8::L * nch * ldv;              // V planes (2 buffers)
+  b += static_cast<size_t>(ne) * i8::L * nch * ldr;                  // residue planes
+  b += 2 * sizeof(double) * (static_cast<size_t>(ne) * nlev + ne);   // d, dmax (2 buffers)
+  b += sizeof(double) * nch;                                         // rowmax
+  b += 2 * sizeof(int32_t) * (static_cast<size_t>(ne) * nch + ne);   // shifts, pole flags (2 buffers)
+  b += sizeof(int32_t) * nch + sizeof(int2) * 4096 + 32 * 1024;      // t_j, tile list, alignment slack
+  return b;
+}
+
+// Two-stream pipeline: the fixed-point conversion of chunk c+1 (ALU + HBM bound, aux stream) runs
+// while the INT8 GEMMs of chunk c (tensor cores, whose warps leave the ALUs idle) run on st;
+// V / d / shifts / pole flags are double-buffered, events order the reuse.
+cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, int64_t nch, int64_t nlev,
+                              double a, const double *E, int64_t ne, double *R, int32_t *status, void *ws,
+                              size_t ws_bytes, int64_t chunk, const Int8Streams &ss, cudaStream_t st,
+                              std::string &err, const std::function<void(bool)> &gemm_mark) {
+  cudaError_t ce = init_i8_consts();
+  if (ce != cudaSuccess) return ce;
+  static bool attr = false;
+  if (!attr) {
+    ce = cudaFuncSetAttribute(i8::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::GEMM_SMEM);
+    if (ce != cudaSuccess) return ce;
+    attr = true;
+  }
+  const int64_t ldv = rint8_ldv(nlev), ldr = rint8_ldr(nch);
+  uint8_t *wsp = static_cast<uint8_t *>(ws);
+  auto carve = [&](size_t bytes) {
+    uint8_t *p = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(wsp) + 255) & ~uintptr_t(255));
+    wsp = p + ((bytes + 255) & ~size_t(255));
+    return p;
+  };
+  int8_t *U = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(i8::L) * nch * ldv));
+  int8_t *V[2];
+  double *dbuf[2], *dmax[2];
+  int32_t *sx[2], *pflag[2];
+  for (int b = 0; b < 2; ++b) {
+    V[b] = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(chunk) * i8::L * nch * ldv));
+    dbuf[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk * nlev));
+    dmax[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk));
+    sx[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk * nch));
+    pflag[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk));
+  }
+  uint8_t *res = carve(static_cast<size_t>(chunk) * i8::L * nch * ldr);
+  double *rowmax = reinterpret_cast<double *>(carve(sizeof(double) * nch));
+  int32_t *tw = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * nch));
+  int2 *tiles = reinterpret_cast<int2 *>(carve(sizeof(int2) * 4096));
+  if (static_cast<size_t>(wsp - static_cast<uint8_t *>(ws)) > ws_bytes) {
+    err = "rform int8: workspace too small";
+    return cudaErrorInvalidValue;
+  }
+
+  // upper-triangle tile list (rows I*128, columns J*256) - static per nch
+  std::vector<int2> tl;
+  for (int I = 0; I * i8::BM < nch; ++I)
+    for (int J = 0; J * i8::BN < nch; ++J)
+      if (J * i8::BN + i8::BN - 1 >= I * i8::BM) tl.push_back(make_int2(I, J));
+  if (tl.size() > 4096) {
+    err = "rform int8: nch too large for the tile list";
+    return cudaErrorInvalidValue;
+  }
+  ce = cudaMemcpyAsync(tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) return ce;
+  const int ntiles = static_cast<int>(tl.size());
+
+  // W operand: row maxima, W' residues, t_j (on st)
+  i8::oz_rowmax_kernel<<<static_cast<unsigned>(nch), 256, 0, st>>>(w, ldw, static_cast<int>(nlev), rowmax);
+  {
+    dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
+    i8::oz_convert_kernel<<<g, 256, 0, st>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev), 1, nullptr,
+                                             nullptr, rowmax, i8::BW, ldv, U, tw);
+  }
+  CUtensorMap tu, tv[2];
+  if (!encode_i8(&tu, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, i8::BN, err)) return cudaErrorInvalidValue;
+  for (int b = 0; b < 2; ++b)
+    if (!encode_i8(&tv[b], V[b], chunk * i8::L * nch, nlev, ldv, i8::BM, err)) return cudaErrorInvalidValue;
+  const double inv2a = 1.0 / (2.0 * a);
+  // the aux stream starts after everything already queued on st (rowmax, inputs)
+  cudaEventRecord(ss.start, st);
+  cudaStreamWaitEvent(ss.aux, ss.start, 0);
+  const int64_t nchunks = (ne + chunk - 1) / chunk;
+  auto convert = [&](int64_t c) {
+    const int b = static_cast<int>(c & 1);
+    const int64_t e0 = c * chunk, n = std::min(chunk, ne - e0);
+    if (c >= 2) cudaStreamWaitEvent(ss.aux, ss.gemm_done[b], 0);  // buffer b free again
+    int32_t *stc = status ? status + e0 : nullptr;
+    i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, ss.aux>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
+                                                                      dmax[b], pflag[b], stc);
+    dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
+    i8::oz_convert_kernel<<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
+                                                 static_cast<int>(n), dbuf[b], dmax[b], rowmax, i8::BX, ldv, V[b],
+                                                 sx[b]);
+    cudaEventRecord(ss.conv_done[b], ss.aux);
+  };
+  convert(0);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int b = static_cast<int>(c & 1);
+    const int64_t e0 = c * chunk, n = std::min(chunk, ne - e0);
+    if (c + 1 < nchunks) convert(c + 1);
+    cudaStreamWaitEvent(st, ss.conv_done[b], 0);
+    gemm_mark(true);
+    i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
+        tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res);
+    gemm_mark(false);
+    dim3 gc(static_cast<unsigned>((nch + 1 + 255) / 256), static_cast<unsigned>((nch + 1) / 2),
+            static_cast<unsigned>(n));
+    i8::oz_crt_kernel<<<gc, 256, 0, st>>>(res, ldr, static_cast<int>(nch), sx[b], tw, inv2a, pflag[b],
+                                          R + e0 * nch * nch);
+    cudaEventRecord(ss.gemm_done[b], st);  // after the CRT: it reads sx[b] and pflag[b]
+    ce = cudaGetLastError();
+    if (ce != cudaSuccess) return ce;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace rmx

@@ -48,12 +48,16 @@ struct rmx_ctx {
   Dev dV, dwork, dinfo;
   // photoionisation amplitudes g of one sweep batch and the split-K partials (NEXT-1)
   Dev dg, dgpart;
+  // R-formation algorithm (RMX_R_DMMA / RMX_R_INT8) and the INT8-CRT workspace
+  int r_algo = RMX_R_DMMA;
+  Dev dz;
+  Int8Streams i8s;
   // instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> free_events;
   std::vector<PendingTiming> pending;
-  double ms[RMX_NKID] = {0, 0, 0, 0};
-  int64_t cnt[RMX_NKID] = {0, 0, 0, 0};
+  double ms[RMX_NKID] = {0, 0, 0, 0, 0};
+  int64_t cnt[RMX_NKID] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
 };
 
@@ -231,9 +235,15 @@ rmx_rc rmx_destroy(rmx_ctx *c) {
   cudaFree(c->match_views);
   cudaFree(c->tepi_views);
   for (auto *d : {&c->dw, &c->dEk, &c->dE, &c->dF, &c->dG, &c->dFp, &c->dGp, &c->dno, &c->drs,
-                  &c->dst, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg, &c->dgpart})
+                  &c->dst, &c->dpart, &c->dV, &c->dwork, &c->dinfo, &c->dg, &c->dgpart, &c->dz})
     cudaFree(d->p);
   if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->i8s.aux) {
+    cudaStreamDestroy(c->i8s.aux);
+    for (cudaEvent_t ev : {c->i8s.start, c->i8s.conv_done[0], c->i8s.conv_done[1], c->i8s.gemm_done[0],
+                           c->i8s.gemm_done[1]})
+      cudaEventDestroy(ev);
+  }
   if (c->blas) cublasDestroy(c->blas);
   delete c;
   return RMX_OK;
@@ -246,6 +256,43 @@ rmx_rc rmx_set_stream(rmx_ctx *c, void *stream) {
 }
 
 const char *rmx_last_error(const rmx_ctx *c) { return c ? c->err.c_str() : "null ctx"; }
+
+// R formation with the context's algorithm; returns the number of kernel launches in *nl
+static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
+                          int64_t nlev, double a, const double *E, int64_t ne, double *R, int32_t *status,
+                          std::string &err, int *nl) {
+  if (c->r_algo == RMX_R_INT8 && nlev <= rint8_max_nlev()) {
+    const int64_t chunk = std::min<int64_t>(ne, kInt8Chunk);
+    const size_t need = rint8_ws_bytes(nch, nlev, chunk);
+    if (grow(c, c->dz, need) != RMX_OK) {
+      err = "INT8-CRT workspace allocation failed";
+      return cudaErrorMemoryAllocation;
+    }
+    if (!c->i8s.aux) {
+      cudaStreamCreateWithFlags(&c->i8s.aux, cudaStreamNonBlocking);
+      for (cudaEvent_t *ev : {&c->i8s.start, &c->i8s.conv_done[0], &c->i8s.conv_done[1], &c->i8s.gemm_done[0],
+                              &c->i8s.gemm_done[1]})
+        cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    }
+    *nl = 2 + 4 * static_cast<int>((ne + chunk - 1) / chunk);
+    cudaEvent_t ga = nullptr;
+    auto mark = [&](bool begin) {  // events around each INT8 GEMM launch (instrumentation only)
+      if (!c->timing) return;
+      cudaEvent_t ev = get_event(c);
+      cudaEventRecord(ev, c->stream);
+      if (begin) {
+        ga = ev;
+      } else {
+        c->pending.push_back({RMX_KID_I8GEMM, ga, ev});
+        c->cnt[RMX_KID_I8GEMM] += 1;
+      }
+    };
+    return launch_rform_int8(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->dz.p, c->dz.bytes, chunk, c->i8s,
+                             c->stream, err, mark);
+  }
+  *nl = 1;
+  return launch_rform(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->stream, err);
+}
 
 rmx_rc rmx_build_R(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
                    int64_t nlev, double a, const double *E, int64_t ne, double *R,
@@ -260,9 +307,12 @@ rmx_rc rmx_build_R(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, i
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
   std::string err;
-  cudaError_t e = timed(c, RMX_KID_RFORM, 1, [&] {
-    return launch_rform(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->stream, err);
+  int nl = 1;
+  cudaError_t e = timed(c, RMX_KID_RFORM, 0, [&] {
+    return form_R(c, w, ldw, Ek, nch, nlev, a, E, ne, R, status, err, &nl);
   });
+  c->launches += nl;
+  c->cnt[RMX_KID_RFORM] += nl;
   if (e != cudaSuccess) {
     if (!err.empty()) return fail(c, RMX_ECUDA, "rmx_build_R: " + err);
     return cuda_fail(c, e, "rmx_build_R");
@@ -403,9 +453,12 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
     const int64_t nb = std::min(batch, ne - b0);
     int32_t *stb = status ? status + b0 : nullptr;
     const int32_t *nob = n_open ? n_open + b0 : nullptr;
-    cudaError_t e = timed(c, RMX_KID_RFORM, 1, [&] {
-      return launch_rform(w, ldw, Ek, nch, nlev, a, E + b0, nb, rb, stb, c->stream, err);
+    int nl = 1;
+    cudaError_t e = timed(c, RMX_KID_RFORM, 0, [&] {
+      return form_R(c, w, ldw, Ek, nch, nlev, a, E + b0, nb, rb, stb, err, &nl);
     });
+    c->launches += nl;
+    c->cnt[RMX_KID_RFORM] += nl;
     if (e != cudaSuccess) return err.empty() ? cuda_fail(c, e, "rmx_sweep/R") : fail(c, RMX_ECUDA, err);
     for (int64_t d = 0; d < n_dump; ++d)
       if (R_d && dump_idx[d] >= b0 && dump_idx[d] < b0 + nb)
@@ -733,6 +786,13 @@ rmx_rc rmx_sync(rmx_ctx *c, const int32_t *status, int64_t ne, int64_t *n_bad) {
       for (auto s : h) *n_bad += (s != 0);
     }
   }
+  return RMX_OK;
+}
+
+rmx_rc rmx_set_r_algo(rmx_ctx *c, int algo) {
+  if (!c) return RMX_EINVAL;
+  if (algo != RMX_R_DMMA && algo != RMX_R_INT8) return fail(c, RMX_EINVAL, "rmx_set_r_algo: unknown algorithm");
+  c->r_algo = algo;
   return RMX_OK;
 }
 

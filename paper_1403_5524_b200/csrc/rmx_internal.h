@@ -1,6 +1,7 @@
 // rmx_internal.h - launcher declarations shared by the librmx translation units (not installed).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 #include <cuda.h>
@@ -52,6 +53,22 @@ cudaError_t launch_rform(const double *w, int64_t ldw, const double *Ek, int64_t
 // SWIZZLE_128B, zero fill out of range)
 bool encode_tmap_f64(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, int64_t ld,
                      int box_rows, std::string &err);
+
+// rint8.cu: R formation on the INT8 tensor cores by CRT (exact integer arithmetic after a 55/53-bit
+// fixed-point rounding of X = W diag(d) and W); ws: rint8_ws_bytes(nch, nlev, chunk) bytes
+constexpr int64_t kInt8Chunk = 8;  // energies per INT8-CRT pass (V planes: 16 nch nlev bytes each)
+int64_t rint8_ldv(int64_t nlev);
+int64_t rint8_ldr(int64_t nch);
+int rint8_max_nlev();
+size_t rint8_ws_bytes(int64_t nch, int64_t nlev, int64_t ne);
+struct Int8Streams {  // auxiliary stream + events of the conversion / GEMM pipeline (owned by the ctx)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t start = nullptr, conv_done[2] = {nullptr, nullptr}, gemm_done[2] = {nullptr, nullptr};
+};
+cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, int64_t nch, int64_t nlev,
+                              double a, const double *E, int64_t ne, double *R, int32_t *status, void *ws,
+                              size_t ws_bytes, int64_t chunk, const Int8Streams &ss, cudaStream_t st,
+                              std::string &err, const std::function<void(bool)> &gemm_mark);
 
 // match.cu
 int64_t match_ws_doubles_per_slot(int64_t nch);

@@ -1,0 +1,108 @@
+"""R formation on the INT8 tensor cores by exact CRT (rmx_set_r_algo(RMX_R_INT8), rint8.cu) against
+the long-double oracle: R to the BASELINE.json:5 bar (1e-10 normwise; the fixed-point rounding of
+X = W diag(d) and W leaves ~1e-14), bitwise symmetry, pole energies, ragged shapes; then the whole
+R -> K -> |T|^2 sweep with INT8 R at the same bars as the DMMA path; and a full darc bench block
+sampled against the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import rmx_synth as syn
+
+pytestmark = pytest.mark.gpu
+
+
+def nrel(x, ref):
+    den = np.max(np.abs(ref))
+    return float(np.max(np.abs(x - ref)) / (den if den > 0 else 1.0))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_1403_5524_b200 as rmx
+    c = rmx.Context()
+    c.set_r_algo(rmx.R_INT8)
+    return c
+
+
+@pytest.mark.parametrize("nch,nlev,seed", [(150, 1000, 1), (203, 517, 2), (37, 77, 3), (1, 5, 4),
+                                           (129, 257, 6), (300, 2100, 7)])
+def test_int8_R_matches_oracle(ctx, nch, nlev, seed):
+    import torch
+    c = syn.brute_force_case(nch, nlev, seed, ne=11, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
+    R, st = ctx.build_R(c.w, c.Ek, c.a, c.E)
+    torch.cuda.synchronize()
+    R = R.cpu().numpy()
+    assert np.all(st.cpu().numpy() == 0)
+    assert np.array_equal(R, np.swapaxes(R, 1, 2))
+    worst = 0.0
+    for p, E in enumerate(c.E):
+        ref, _ = oracle.R(c.w, c.Ek, c.a, E)
+        worst = max(worst, nrel(R[p], ref))
+    assert worst < 1e-12, worst
+
+
+def test_int8_pole_status(ctx):
+    import torch
+    c = syn.brute_force_case(40, 100, 9, ne=4, lo=1.0, hi=5.0)
+    E = np.array([c.Ek[50], 2.5])
+    R, st = ctx.build_R(c.w, c.Ek, c.a, E)
+    torch.cuda.synchronize()
+    assert st.cpu().numpy().tolist() == [1, 0]
+    assert torch.isnan(R[0]).all() and torch.isfinite(R[1]).all()
+
+
+def test_int8_sweep_parity(ctx):
+    """The fused sweep with INT8 R: K_oo and |T|^2 / row sums to the 1e-10 / 1e-8 bars."""
+    import torch
+    c = syn.brute_force_case(160, 900, 13, ne=10, lo=0.5, hi=9.0, a=12.0, eps_hi=3.0)
+    F, G, Fp, Gp = syn.asymptotic(c.eps, c.E, c.a)
+    no = syn.n_open(c.eps, c.E)
+    out = ctx.sweep(c.w, c.Ek, c.a, c.E, F, G, Fp, Gp, no, batch=4, dump_idx=list(range(c.ne)))
+    torch.cuda.synchronize()
+    ref = oracle.sweep(c.w, c.Ek, c.a, c.E, F, G, Fp, Gp, no, np.arange(c.ne))
+    for p in range(c.ne):
+        o = int(no[p])
+        assert nrel(out["R"][p].cpu().numpy(), ref["R"][p]) < 1e-12
+        if o:
+            assert nrel(out["K"][p].cpu().numpy()[:o, :o], ref["K"][p][:o, :o]) < 1e-10
+        assert nrel(out["T2"][p].cpu().numpy(), ref["T2"][p]) < 1e-8
+        assert nrel(out["rowsum"][p].cpu().numpy(), ref["rowsum"][p]) < 1e-8
+
+
+def test_int8_darc_block(ctx):
+    """darc (nch 2000, nlev 40000) in the bench launch configuration: INT8 R of 296 energies against the
+    DMMA R (both fp64-accurate) and sampled oracle entries."""
+    import torch
+    import paper_1403_5524_b200 as rmx
+    c = syn.make_case("darc")
+    E = c.E[50000:50000 + 296]
+    dump = [0, 100, 295]
+    F, G, Fp, Gp = syn.asymptotic(c.eps, E, c.a)
+    no = syn.n_open(c.eps, E)
+    out8 = ctx.sweep(c.w, c.Ek, c.a, E, F, G, Fp, Gp, no, batch=296, dump_idx=dump)
+    ctx64 = rmx.Context()
+    out64 = ctx64.sweep(c.w, c.Ek, c.a, E, F, G, Fp, Gp, no, batch=296, dump_idx=dump)
+    torch.cuda.synchronize()
+    assert int((out8["status"] != 0).sum()) == 0
+    rng = np.random.default_rng(0)
+    for d, l in enumerate(dump):
+        R8, R64 = out8["R"][d].cpu().numpy(), out64["R"][d].cpu().numpy()
+        assert nrel(R8, R64) < 1e-12, nrel(R8, R64)
+        ii, jj = rng.integers(0, c.nch, 40), rng.integers(0, c.nch, 40)
+        vals, st = oracle.R_entries(c.w, c.Ek, c.a, E[l], ii, jj)
+        assert np.max(np.abs(R8[ii, jj] - vals)) / np.max(np.abs(R8)) < 1e-12
+        o = int(no[l])
+        assert nrel(out8["T2"][d].cpu().numpy(), out64["T2"][d].cpu().numpy()) < 1e-8
+    # row sums of all 296 energies: INT8 and DMMA R agree to the |T|^2 bar except where the matching is
+    # ill-conditioned; there both are as far from the oracle (the R rounding of either path is
+    # amplified the same way), which is checked at the worst energy
+    rs8, rs64 = out8["rowsum"].cpu().numpy(), out64["rowsum"].cpu().numpy()
+    per = np.max(np.abs(rs8 - rs64), axis=1) / np.max(np.abs(rs64), axis=1)
+    assert np.median(per) < 1e-10 and np.sum(per > 1e-8) <= 0.05 * len(E), np.sort(per)[-5:]
+    l = int(np.argmax(per))
+    if per[l] > 1e-8:
+        ref = oracle.sweep(c.w, c.Ek, c.a, E[l:l + 1], F[l:l + 1], G[l:l + 1], Fp[l:l + 1], Gp[l:l + 1],
+                           no[l:l + 1], np.arange(1), want=("rowsum",))["rowsum"][0]
+        e8, e64 = nrel(rs8[l], ref), nrel(rs64[l], ref)
+        assert e8 <= 2.0 * e64 + 1e-9, (l, e8, e64)
