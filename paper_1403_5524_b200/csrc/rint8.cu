@@ -8,9 +8,9 @@
 //      s_i from the bound max_k|w_ik| dmax;  W'_jk = rint(w_jk 2^{t_j}),  |W'| <= 2^52.
 //      Then P_ij = sum_k X'_ik W'_jk is an exact integer, |P| <= nlev 2^106 < M/2 for nlev < 2^17,
 //      M = prod of the 16 pairwise-coprime moduli below (2^125.19).
-//   3. For each modulus m_l: V_l = X' mod m_l, U_l = W' mod m_l as signed int8 (|.| <= 128); the INT8
-//      tensor-core GEMM C_l = V_l U_l^T is exact in int32 (|C| <= 128^2 nlev < 2^31), its residue
-//      C_l mod m_l = P mod m_l.
+//   3. For each modulus m_l: V_l = X' mod m_l (uint8 in [0, m); balanced int8 when nlev > 65000),
+//      U_l = W' mod m_l as balanced int8 (|.| <= 128); the INT8 tensor-core GEMM C_l = V_l U_l^T is
+//      exact in int32 (|C| <= 255 * 128 nlev < 2^31), its residue C_l mod m_l = P mod m_l.
 //   4. CRT (direct formula, exact 128-bit wrapping arithmetic) recovers P_ij in (-M/2, M/2); then
 //      R_ij = P_ij 2^{-s_i - t_j} / (2a), upper triangle mirrored (bitwise symmetric R).
 // The only approximation is the rounding of X and W to 55 / 53 significant bits relative to the row
@@ -43,6 +43,7 @@ struct ModConst {
   int c36, c18, off;  // 2^36 mod m, 2^18 mod m, (m * 2^10 - (2^BIAS mod m)) so that s stays >= 0
   float inv;          // 1/m (rounded down a little: q never overestimates by more than 1)
   uint32_t magic;     // ceil(2^32 / m): umulhi(s, magic) is floor(s/m) or one more for s < 2^28
+  uint32_t m36;       // ceil(2^36 / m): umulhi(s, m36) >> 4 == floor(s/m) exactly for s < 2^28, m < 256
 };
 __constant__ ModConst c_mod[L];
 
@@ -124,6 +125,11 @@ __global__ void __launch_bounds__(256) oz_rowmax_kernel(const double *__restrict
 // consecutive k, its 8 w values loaded once and reused for all ne energies of the chunk.
 // dbuf == nullptr: the W operand (d = 1, BW bits, ne = 1); else the X operands of energies 0..ne-1.
 // out: planes [ne][L][nch][ldv] int8 (ldv multiple of 16); shift: [ne][nch] exponents s_i / t_j.
+// SIGNED: balanced residues in [-(m-1)/2, (m-1)/2] (int8; needed when nlev > 65000), else plain
+// residues in [0, m) (uint8 operand: u8 x s8 products stay < 2^31 summed over nlev <= 65000).
+// Per residue: s = u2 c36 + u1 c18 + u0 + off (< 2^28), q = umulhi(s, ceil(2^36/m)) >> 4 (exact),
+// r = s - q m. The modulus 256 residue is the low byte of the two's-complement value.
+template <bool SIGNED>
 __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restrict__ w, int64_t ldw, int nch,
                                                          int nlev, int ne, const double *__restrict__ dbuf,
                                                          const double *__restrict__ dmax,
@@ -161,16 +167,23 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
       u0[q] = static_cast<uint32_t>(u & 0x3FFFF);
     }
     int8_t *o = out + static_cast<int64_t>(e) * L * plane + static_cast<int64_t>(i) * ldv + k0;
+    {  // modulus 256: the low byte (u = X' + 2^54, 2^54 = 0 mod 256)
+      uint32_t pk[2] = {0u, 0u};
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
+      for (int q = 0; q < 8; ++q) pk[q >> 2] |= (u0[q] & 0xFFu) << (8 * (q & 3));
+      *reinterpret_cast<uint2 *>(o) = make_uint2(pk[0], pk[1]);
+    }
+#pragma unroll
+    for (int l = 1; l < L; ++l) {
       const int m = mod_of(l);
       const ModConst mc = c_mod[l];
       uint32_t pk[2] = {0u, 0u};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t sv = u2[q] * mc.c36 + u1[q] * mc.c18 + u0[q] + mc.off;
-        const int r = umod_magic(sv, m, mc.magic);
-        pk[q >> 2] |= (static_cast<uint32_t>(static_cast<uint8_t>(bal(r, m))) << (8 * (q & 3)));
+        int r = static_cast<int>(sv - (__umulhi(sv, mc.m36) >> 4) * m);
+        if (SIGNED) r -= (r > (m - 1) / 2) ? m : 0;
+        pk[q >> 2] |= (static_cast<uint32_t>(r) & 0xFFu) << (8 * (q & 3));
       }
       *reinterpret_cast<uint2 *>(o + l * plane) = make_uint2(pk[0], pk[1]);
     }
@@ -185,8 +198,11 @@ constexpr int BM = 128, BN = 256, BKB = 128, STAGES = 4;
 constexpr int A_BYTES = BM * BKB, B_BYTES = BN * BKB, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int GEMM_NT = 256;
 constexpr int GEMM_SMEM = 1024 + STAGES * STAGE_BYTES + 256;
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                           (static_cast<uint32_t>(BM >> 4) << 24);
+// instruction descriptor: s32 accumulate, A u8 (plain residues) or s8 (balanced), B s8, K-major, M 128, N 256
+__host__ __device__ constexpr uint32_t idesc_i8(bool a_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+         (static_cast<uint32_t>(BM >> 4) << 24);
+}
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
@@ -199,7 +215,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 
 __global__ void __launch_bounds__(GEMM_NT, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu, int nch,
-                   int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res) {
+                   int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res,
+                   uint32_t idesc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
@@ -256,7 +273,7 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
         const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(IDESC), "r"(acc));
+                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                        smem_u32(&empty[s]))
@@ -408,6 +425,7 @@ static cudaError_t init_i8_consts() {
     mc[l].off = static_cast<int>(m * 1024 - static_cast<int>(p54));
     mc[l].inv = nextafterf(1.0f / static_cast<float>(m), 0.0f);
     mc[l].magic = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 32) + m - 1) / m);
+    mc[l].m36 = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 36) + m - 1) / m);
     // C_l = (M/m) * ((M/m)^-1 mod m)
     const unsigned __int128 Ml = M / static_cast<unsigned>(m);
     const int Mlm = static_cast<int>(Ml % static_cast<unsigned>(m));
@@ -533,14 +551,17 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   i8::oz_rowmax_kernel<<<static_cast<unsigned>(nch), 256, 0, st>>>(w, ldw, static_cast<int>(nlev), rowmax);
   {
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
-    i8::oz_convert_kernel<<<g, 256, 0, st>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev), 1, nullptr,
-                                             nullptr, rowmax, i8::BW, ldv, U, tw);
+    i8::oz_convert_kernel<true><<<g, 256, 0, st>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev), 1,
+                                                   nullptr, nullptr, rowmax, i8::BW, ldv, U, tw);
   }
   CUtensorMap tu, tv[2];
   if (!encode_i8(&tu, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, i8::BN, err)) return cudaErrorInvalidValue;
   for (int b = 0; b < 2; ++b)
     if (!encode_i8(&tv[b], V[b], chunk * i8::L * nch, nlev, ldv, i8::BM, err)) return cudaErrorInvalidValue;
   const double inv2a = 1.0 / (2.0 * a);
+  // plain (unsigned) X residues keep |C| <= 255 * 128 * nlev < 2^31 up to nlev = 65793
+  const bool x_signed = nlev > 65000;
+  const uint32_t idesc = i8::idesc_i8(x_signed);
   // the aux stream starts after everything already queued on st (rowmax, inputs)
   cudaEventRecord(ss.start, st);
   cudaStreamWaitEvent(ss.aux, ss.start, 0);
@@ -553,9 +574,14 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, ss.aux>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
                                                                       dmax[b], pflag[b], stc);
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
-    i8::oz_convert_kernel<<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
-                                                 static_cast<int>(n), dbuf[b], dmax[b], rowmax, i8::BX, ldv, V[b],
-                                                 sx[b]);
+    if (x_signed)
+      i8::oz_convert_kernel<true><<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
+                                                         static_cast<int>(n), dbuf[b], dmax[b], rowmax, i8::BX, ldv,
+                                                         V[b], sx[b]);
+    else
+      i8::oz_convert_kernel<false><<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
+                                                          static_cast<int>(n), dbuf[b], dmax[b], rowmax, i8::BX,
+                                                          ldv, V[b], sx[b]);
     cudaEventRecord(ss.conv_done[b], ss.aux);
   };
   convert(0);
@@ -566,7 +592,7 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     cudaStreamWaitEvent(st, ss.conv_done[b], 0);
     gemm_mark(true);
     i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
-        tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res);
+        tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc);
     gemm_mark(false);
     dim3 gc(static_cast<unsigned>((nch + 1 + 255) / 256), static_cast<unsigned>((nch + 1) / 2),
             static_cast<unsigned>(n));

@@ -106,3 +106,20 @@ def test_int8_darc_block(ctx):
                            no[l:l + 1], np.arange(1), want=("rowsum",))["rowsum"][0]
         e8, e64 = nrel(rs8[l], ref), nrel(rs64[l], ref)
         assert e8 <= 2.0 * e64 + 1e-9, (l, e8, e64)
+
+
+def test_int8_many_poles_signed_residues(ctx):
+    """nlev > 65000 switches the X residues to balanced int8 (the u8 x s8 accumulator bound): R still
+    matches the oracle."""
+    import torch
+    rng = np.random.default_rng(5)
+    nch, nlev = 40, 70001
+    Ek = np.sort(rng.uniform(-5.0, 300.0, nlev))
+    w = rng.normal(0.0, 0.05, (nch, nlev))
+    E = np.array([0.7, 13.3, 57.9])
+    R, st = ctx.build_R(w, Ek, 12.0, E)
+    torch.cuda.synchronize()
+    R = R.cpu().numpy()
+    for p, x in enumerate(E):
+        ref, _ = oracle.R(w, Ek, 12.0, x)
+        assert nrel(R[p], ref) < 1e-12, (x, nrel(R[p], ref))
