@@ -375,14 +375,17 @@ def main():
             peak_i8 = 2.0 * float(pk.get("bf16_tflops_sustained", 1378.4))
             ops_i8 = 16.0 * fr
             ach_i8 = ops_i8 / (ms_g / 1e3) / 1e12 if ms_g > 0 else None
-            traffic, traffic_src = ncu_traffic(args.config, batch, kernel="oz_gemm")
+            # DRAM bytes per GEMM launch (one chunk of 8 energies: librmx kInt8Chunk)
+            traffic, traffic_src = ncu_traffic(args.config, min(batch, 8), kernel="oz_gemm")
             roofline = {"bound": "tensor", "kernel": "oz_gemm_kernel (INT8 tcgen05, 16 moduli, CRT R formation)",
                         "achieved": ach_i8, "peak": peak_i8, "unit": "TOPS",
                         "frac": (ach_i8 / peak_i8) if ach_i8 else None,
                         "traffic": traffic, "traffic_source": traffic_src,
                         "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (nominal int8/bf16 ratio, "
                                        "B200_PROFILING.md); nominal dense int8 4500 TOPS",
-                        "algorithmic": "16 x nch(nch+1) x nlev int8 ops per energy x energies per launch"}
+                        "algorithmic": "16 x nch(nch+1) x nlev int8 ops per energy x energies per launch",
+                        "traffic_per": "one oz_gemm launch = 8 energies (algorithmic bytes: 8 x 16 x nch x nlev "
+                                       "X residues + 16 x nch x nlev W residues)"}
             r_form = {"algo": "int8-crt (rint8.cu)", "fp64_equivalent_tflops": achieved_r,
                       "vs_fp64_dmma_peak": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,
                       "i8gemm_ms": round(ms_g, 3), "rform_total_ms": round(ms_r, 3)}

@@ -216,7 +216,7 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 __global__ void __launch_bounds__(GEMM_NT, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu, int nch,
                    int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res,
-                   uint32_t idesc) {
+                   uint32_t idesc, int nen) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
@@ -224,9 +224,11 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
   uint64_t *accf = empty + STAGES;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
   const int warp = warp_id(), lane = lane_id();
+  // tiles fastest, then energies, then moduli: the GEMMs resident together share U_l (one modulus's W
+  // residues) through L2 and differ only in their X residues
   const int tile = blockIdx.x % ntiles;
-  const int l = (blockIdx.x / ntiles) % L;
-  const int64_t e = blockIdx.x / (ntiles * L);
+  const int64_t e = (blockIdx.x / ntiles) % nen;
+  const int l = blockIdx.x / (ntiles * nen);
   const int2 tij = tiles[tile];  // (I, J): rows I*128.., columns J*256..
   const int nk = (nlev + BKB - 1) / BKB;
   const int vrow = static_cast<int>((e * L + l) * nch) + tij.x * BM;  // row in the stacked V planes
@@ -592,7 +594,8 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     cudaStreamWaitEvent(st, ss.conv_done[b], 0);
     gemm_mark(true);
     i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
-        tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc);
+        tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc,
+        static_cast<int>(n));
     gemm_mark(false);
     dim3 gc(static_cast<unsigned>((nch + 1 + 255) / 256), static_cast<unsigned>((nch + 1) / 2),
             static_cast<unsigned>(n));
