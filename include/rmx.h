@@ -305,7 +305,8 @@ rmx_rc rmx_sync(rmx_ctx *ctx, const int32_t *status, int64_t ne, int64_t *n_bad)
  *   RMX_R_INT8: the same R by exact integer arithmetic on the INT8 tensor cores (tcgen05 kind::i8):
  *     X = W diag(d) and W rounded to 55 / 53-bit fixed point per row, 16 modular INT8 GEMMs, CRT
  *     reconstruction (rint8.cu); R error at the level of an fp64 contraction
- *     (normwise ~1e-14). Needs nlev <= 131071 (int32 accumulator bound), else DMMA is used.
+ *     (normwise ~1e-14). Applies for nch >= 256 and nlev <= 131071 (int32 accumulator bound);
+ *     otherwise the DMMA contraction is used.
  *     Workspace ~ 8 x 16 x nch x nlev bytes.
  */
 enum { RMX_R_DMMA = 0, RMX_R_INT8 = 1 };

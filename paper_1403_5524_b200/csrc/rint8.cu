@@ -264,18 +264,23 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
       tma_load_2d(base + A_BYTES, &tu, &full[s], kt * BKB, urow);
     }
   } else if (warp == 1 && lane == 0) {
+    const bool half = tij.y * BN + 127 < tij.x * BM;
+    const uint32_t idesc_k = half ? ((idesc & ~(0x3Fu << 17)) | (static_cast<uint32_t>(128 >> 3) << 17)) : idesc;
     for (int kt = 0; kt < nk; ++kt) {
       const int s = kt % STAGES;
       mbar_wait(&full[s], (kt / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-      const uint64_t da = umma_desc_sw128(base), db = umma_desc_sw128(base + A_BYTES);
+      // a tile whose first 128 columns lie entirely below the diagonal computes only its right half
+      // (N = 128 into TMEM columns 128..255; the left half's residues are never read by the CRT)
+      const uint32_t boff = half ? static_cast<uint32_t>(128 * BKB) : 0u;
+      const uint64_t da = umma_desc_sw128(base), db = umma_desc_sw128(base + A_BYTES + boff);
 #pragma unroll
       for (int k = 0; k < BKB / 32; ++k) {
         const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (half ? 128u : 0u)),
+                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc_k), "r"(acc));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                        smem_u32(&empty[s]))

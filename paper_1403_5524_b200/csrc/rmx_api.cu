@@ -261,7 +261,7 @@ const char *rmx_last_error(const rmx_ctx *c) { return c ? c->err.c_str() : "null
 static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double *Ek, int64_t nch,
                           int64_t nlev, double a, const double *E, int64_t ne, double *R, int32_t *status,
                           std::string &err, int *nl) {
-  if (c->r_algo == RMX_R_INT8 && nlev <= rint8_max_nlev()) {
+  if (c->r_algo == RMX_R_INT8 && nlev <= rint8_max_nlev() && nch >= kInt8MinChannels) {
     const int64_t chunk = std::min<int64_t>(ne, kInt8Chunk);
     const size_t need = rint8_ws_bytes(nch, nlev, chunk);
     if (grow(c, c->dz, need) != RMX_OK) {

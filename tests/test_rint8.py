@@ -25,8 +25,8 @@ def ctx():
     return c
 
 
-@pytest.mark.parametrize("nch,nlev,seed", [(150, 1000, 1), (203, 517, 2), (37, 77, 3), (1, 5, 4),
-                                           (129, 257, 6), (300, 2100, 7)])
+@pytest.mark.parametrize("nch,nlev,seed", [(300, 1000, 1), (403, 517, 2), (257, 77, 3), (256, 5, 4),
+                                           (529, 257, 6), (300, 2100, 7)])
 def test_int8_R_matches_oracle(ctx, nch, nlev, seed):
     import torch
     c = syn.brute_force_case(nch, nlev, seed, ne=11, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
@@ -44,7 +44,7 @@ def test_int8_R_matches_oracle(ctx, nch, nlev, seed):
 
 def test_int8_pole_status(ctx):
     import torch
-    c = syn.brute_force_case(40, 100, 9, ne=4, lo=1.0, hi=5.0)
+    c = syn.brute_force_case(260, 300, 9, ne=4, lo=1.0, hi=5.0)
     E = np.array([c.Ek[50], 2.5])
     R, st = ctx.build_R(c.w, c.Ek, c.a, E)
     torch.cuda.synchronize()
@@ -55,7 +55,7 @@ def test_int8_pole_status(ctx):
 def test_int8_sweep_parity(ctx):
     """The fused sweep with INT8 R: K_oo and |T|^2 / row sums to the 1e-10 / 1e-8 bars."""
     import torch
-    c = syn.brute_force_case(160, 900, 13, ne=10, lo=0.5, hi=9.0, a=12.0, eps_hi=3.0)
+    c = syn.brute_force_case(300, 900, 13, ne=10, lo=0.5, hi=9.0, a=12.0, eps_hi=3.0)
     F, G, Fp, Gp = syn.asymptotic(c.eps, c.E, c.a)
     no = syn.n_open(c.eps, c.E)
     out = ctx.sweep(c.w, c.Ek, c.a, c.E, F, G, Fp, Gp, no, batch=4, dump_idx=list(range(c.ne)))
@@ -113,7 +113,7 @@ def test_int8_many_poles_signed_residues(ctx):
     matches the oracle."""
     import torch
     rng = np.random.default_rng(5)
-    nch, nlev = 40, 70001
+    nch, nlev = 260, 70001
     Ek = np.sort(rng.uniform(-5.0, 300.0, nlev))
     w = rng.normal(0.0, 0.05, (nch, nlev))
     E = np.array([0.7, 13.3, 57.9])
