@@ -367,7 +367,7 @@ def main():
                          f"{dt:.1f} s, OpenMP over rows/energies"}
 
     if rank == 0:
-        if args.r_algo == "int8":
+        if args.r_algo == "int8" and ms_g > 0:  # (nch < 256 falls back to the DMMA R formation)
             # dominant kernel: the INT8 tensor-core GEMMs of the CRT R formation. Algorithmic int8 ops per
             # energy: 16 moduli x nch(nch+1) nlev (upper triangle, like the fp64 count). Peak: the INT8 dense
             # rate = measured bf16 (sustained: the GEMMs run inside a long step) x the nominal int8/bf16 ratio 2.
@@ -404,7 +404,7 @@ def main():
             "value": value, "unit": "energies/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64" if args.r_algo == "dmma" else "f64 (R: exact int8 CRT on tcgen05; K, T: f64 DMMA)",
+            "dtype": "f64" if r_form["algo"].startswith("fp64") else "f64 (R: exact int8 CRT on tcgen05; K, T: f64 DMMA)",
             "data": "synthetic (rmx_synth, seed 0)",
             "config": {"workload": args.config, "nch": nch, "nlev": nlev, "ne_mesh": ne,
                        "a": cfg["a"], "energies_per_step_per_gpu": batch,
@@ -415,7 +415,7 @@ def main():
             "r_formation": r_form,
             "kernel_ms": {k: round(v[0], 3) for k, v in stats.items() if k != "launches"},
             "path_fp64_tflops": path_tflops,
-            ("path_fp64_frac" if args.r_algo == "dmma" else "path_fp64_equivalent_vs_dmma_peak"):
+            ("path_fp64_frac" if r_form["algo"].startswith("fp64") else "path_fp64_equivalent_vs_dmma_peak"):
                 path_tflops / FP64_DMMA_PEAK_TFLOPS,
             "gpu_launches": int(stats["launches"]),
             "bad_status_energies": bad,

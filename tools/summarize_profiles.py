@@ -33,10 +33,12 @@ for r in (rows[hi + 1:] if hi is not None else []):
     a[0] += 1
     a[1] += v
 tot = sum(v[1] for v in agg.values()) or 1.0
-ours = {k: v for k, v in agg.items() if any(s in k for s in ("rform", "match_kernel", "tepi_kernel"))}
+ours = {k: v for k, v in agg.items() if any(s in k for s in ("rform", "match_kernel", "tepi_kernel", "oz_",
+                                                                "dipole_g", "conv_gauss", "maxwell"))}
 tot_ours = sum(v[1] for v in ours.values()) or 1.0
 lines = [f"# Round {rnd} ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-         "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline` (darc, 296 energies/step).",
+         "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline` (darc, 296 energies/step, "
+         "INT8-CRT R formation).",
          "Per-launch times are cold-cache and serialised: compare shares, not absolutes.", "",
          "| kernel | launches | total ms | share of all | share of librmx |", "|---|---|---|---|---|"]
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:15]:
