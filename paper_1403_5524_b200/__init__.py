@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librmx.so")
+LIB_PATH = os.environ.get("RMX_LIB", os.path.join(_PKG, "librmx.so"))
 
 RMX_OK, RMX_EINVAL, RMX_ENOMEM, RMX_ECUDA = 0, 1, 2, 3
 E_OK, E_POLE, E_SINGULAR, E_NONFINITE = 0, 1, 2, 3

@@ -32,6 +32,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def build_phases(verbose: bool = False) -> str:
+    """Diagnostic variant with per-phase clock64 counters in the matching kernel (librmx_phases.so)."""
+    out = os.path.join(PKG, "librmx_phases.so")
+    cmd = [NVCC, *FLAGS, "-DRMX_PHASES", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd, cwd=CSRC)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
@@ -45,5 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    if "--phases" in sys.argv:
+        print(build_phases(verbose=True))
+    else:
+        build(force="--force" in sys.argv, verbose=True)
+        print(LIB)

@@ -12,6 +12,25 @@ namespace rmx {
 
 using namespace la;
 
+#ifdef RMX_PHASES
+// per-phase clock64 totals of block 0 (diagnostic build only: python -m paper_1403_5524_b200.build
+// --phases -> librmx_phases.so; tools/phases.py reads them)
+__device__ unsigned long long g_match_phase[8];
+#define PH_MARK(k)                                                          \
+  do {                                                                      \
+    __syncthreads();                                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      const unsigned long long now_ = clock64();                            \
+      g_match_phase[k] += now_ - ph_t0;                                     \
+      ph_t0 = now_;                                                         \
+    }                                                                       \
+  } while (0)
+#else
+#define PH_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 struct MatchSmem {
   union {  // the triangle scratch is only used between gemm calls
     double gemm[GEMM_SMEM_DOUBLES];
@@ -56,6 +75,9 @@ __global__ void __launch_bounds__(NT, 1)
     const int ncols = npad + o;
     const double *Re = R + e * static_cast<int64_t>(n) * ldr;
     const double *Fe = F + e * n, *Ge = G + e * n, *Fpe = Fp + e * n, *Gpe = Gp + e * n;
+#ifdef RMX_PHASES
+    unsigned long long ph_t0 = clock64();
+#endif
     // unknowns ordered closed channels first, open last: column q of A holds channel
     // jq = (q < nc) ? o + q : q - nc, so the open unknowns are the LAST rows of the triangular
     // solve and back substitution for K_oo can stop after them (SURVEY §8(a) S4 flops:
@@ -97,6 +119,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     __syncthreads();
 
+    PH_MARK(0);  // formation pass
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
     // Outer blocks of W = NB = 128 columns, factored as four 32-wide panels (each followed by a
     // K = 32 update of the block's remaining columns), then U12 = L11^{-1} A12 as ONE in-place DMMA
@@ -117,12 +140,15 @@ __global__ void __launch_bounds__(NT, 1)
                    false, smg, gs);
         }
       }
+      PH_MARK(1);  // panels (panel_lu + in-block K = 32 updates)
       // trailing columns (A part and right-hand sides); when the last block ends on an odd n the
       // zero pad column n is skipped so that every C row stays 16-byte aligned
       const int ct = min((P0 + W + 1) & ~1, ncols);
       const int nt = ncols - ct;
       if (nt > 0) {
+        PH_MARK(2);
         tri_inv128(Mv, P0, W, TRI_UNIT_LOWER, Tv, smg, gs);  // L11^{-1}
+        PH_MARK(5);
         // U12 = L11^{-1} A12 in place: W <= 128 = BM rows, so each output tile column depends only
         // on its own input columns
         gemm_set(W, nt, W, opk(Tv, 0, 0), opn(Mv, P0, ct), Mv, P0, ct, false, 0.0, smg, gs);
@@ -130,6 +156,7 @@ __global__ void __launch_bounds__(NT, 1)
           gemm_sub(n - P0 - W, nt, W, opk(Mv, P0 + W, P0), opn(Mv, P0, ct), Mv, P0 + W, ct, false,
                    smg, gs);
       }
+      PH_MARK(2);  // U12 + K = 128 trailing update
     }
 
     // ---- S4b: blocked back substitution U Y = L^{-1} P B_open (Y = columns [npad, npad+o)) ----
@@ -140,13 +167,16 @@ __global__ void __launch_bounds__(NT, 1)
     if (o > 0) {
       for (int P0 = ((n - 1) / NB) * NB; P0 >= 0 && P0 + NB > rlo; P0 -= NB) {
         const int W = min(NB, n - P0);
+        PH_MARK(3);
         tri_inv128(Mv, P0, W, TRI_UPPER, Tv, smg, gs);  // U_pp^{-1}
+        PH_MARK(6);
         gemm_set(W, o, W, opk(Tv, 0, 0), opn(Mv, P0, npad), Mv, P0, npad, false, 0.0, smg, gs);
         if (P0 > rlo)
           gemm_sub(P0 - rlo, o, W, opk(Mv, rlo, P0), opn(Mv, P0, npad), Mv, rlo, npad, false, smg, gs);
       }
     }
 
+    PH_MARK(3);  // back substitution
     // ---- output: K = -Y (open columns), -e_j (closed columns); status ----
     int bad = 0;
     double *Ke = K + e * static_cast<int64_t>(n) * ldk;
@@ -168,6 +198,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     bad = __syncthreads_or(bad);
+    PH_MARK(4);  // output
     if (threadIdx.x == 0) {
       if (singular)
         set_status(status, e, RMX_E_SINGULAR);
@@ -178,6 +209,13 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 int64_t match_ws_doubles_per_slot(int64_t nch) { return match_layout(nch).slot; }
+
+#ifdef RMX_PHASES
+extern "C" int rmx_debug_match_phases(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_match_phase, sizeof(g_match_phase)));
+}
+#endif
 
 // Matrices of one slot whose TMA descriptors the kernel uses: (M, Tg), NVIEW box shapes each.
 void match_view_specs(int64_t nch, std::vector<MatSpec> &specs) {

@@ -162,27 +162,41 @@ __global__ void __launch_bounds__(MAXW_PAIRS) maxwell_partial_kernel(
 #pragma unroll
   for (int t = 0; t < RMX_MAX_TEMPS; ++t) acc[t] = 0.0;
   bool direct = false;
-  for (int t = 0; t < T.nT; ++t) direct |= (eth - Ec0) / T.kT[t] > 600.0;
-  for (int ii = 0; ii < n; ++ii) {
-    const int64_t i = c0 + ii;
-    const double Ei = sx[ii + 1];
-    if (!(Ei > eth)) continue;  // point not above threshold (E ascending: a prefix of the chunk)
-    // trapezoid weight: half the interval to the right (if any) plus half the interval to the
-    // left when the left neighbour is also above threshold
-    const double right = (i + 1 < ne) ? 0.5 * (sx[ii + 2] - Ei) : 0.0;
-    const double left = (i > 0 && sx[ii] > eth) ? 0.5 * (Ei - sx[ii]) : 0.0;
-    const double om = (right + left) * omega[i * npair + p];
-    if (!direct) {
 #pragma unroll
-      for (int t = 0; t < RMX_MAX_TEMPS; ++t)
-        if (t < T.nT) acc[t] = fma(om, sE[t][ii], acc[t]);
-    } else {
+  for (int t = 0; t < RMX_MAX_TEMPS; ++t) direct |= (t < T.nT) && (eth - Ec0) / T.kT[t] > 600.0;
+  // Omega loads issued in groups of 8 (independent of the accumulation; the loop is latency-bound
+  // otherwise)
+  constexpr int PF = 8;
+  for (int g0 = 0; g0 < n; g0 += PF) {
+    double ob[PF];
 #pragma unroll
-      for (int t = 0; t < RMX_MAX_TEMPS; ++t)
-        if (t < T.nT) acc[t] = fma(om, exp(-(Ei - eth) / T.kT[t]), acc[t]);
+    for (int q = 0; q < PF; ++q) ob[q] = (g0 + q < n) ? omega[(c0 + g0 + q) * npair + p] : 0.0;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int ii = g0 + q;
+      if (ii >= n) break;
+      const int64_t i = c0 + ii;
+      const double Ei = sx[ii + 1];
+      if (!(Ei > eth)) continue;  // point not above threshold (E ascending: a prefix of the chunk)
+      // trapezoid weight: half the interval to the right (if any) plus half the interval to the
+      // left when the left neighbour is also above threshold
+      const double right = (i + 1 < ne) ? 0.5 * (sx[ii + 2] - Ei) : 0.0;
+      const double left = (i > 0 && sx[ii] > eth) ? 0.5 * (Ei - sx[ii]) : 0.0;
+      const double om = (right + left) * ob[q];
+      if (!direct) {
+#pragma unroll
+        for (int t = 0; t < RMX_MAX_TEMPS; ++t)
+          if (t < T.nT) acc[t] = fma(om, sE[t][ii], acc[t]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < RMX_MAX_TEMPS; ++t)
+          if (t < T.nT) acc[t] = fma(om, exp(-(Ei - eth) / T.kT[t]), acc[t]);
+      }
     }
   }
-  for (int t = 0; t < T.nT; ++t) {
+#pragma unroll
+  for (int t = 0; t < RMX_MAX_TEMPS; ++t) {
+    if (t >= T.nT) break;
     const double f = direct ? 1.0 : exp(-(Ec0 - eth) / T.kT[t]);
     part[(c * npair + p) * T.nT + t] = acc[t] * f / T.kT[t];
   }
