@@ -122,14 +122,15 @@ def test_gpu_convolve(ctx, ne, dE, fwhm):
 
 
 @pytest.mark.gpu
-def test_gpu_maxwell(ctx):
+@pytest.mark.parametrize("nT", [7, 20])
+def test_gpu_maxwell(ctx, nT):
     import torch
     rng = np.random.default_rng(4)
-    ne, npair = 5000, 300
+    ne, npair = 5000, 700
     E = 0.5 + np.arange(ne) * (59.5 / (ne - 1))
     Eth = np.sort(rng.uniform(0.0, 50.0, npair))
     om = rng.uniform(0.0, 3.0, (ne, npair)) * (E[:, None] > Eth[None, :])
-    kT = [0.1, 0.5, 1.0, 2.0, 5.0, 20.0, 60.0]
+    kT = list(np.geomspace(0.03, 60.0, nT))
     ups = ctx.maxwell_average(om, E, Eth, kT).cpu().numpy()
     torch.cuda.synchronize()
     ref = oracle.maxwell_average(om, E, Eth, kT)
