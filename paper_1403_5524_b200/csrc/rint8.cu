@@ -5,7 +5,7 @@
 //
 //   1. d_k(E) = 1/(E_k - E) and dmax(E) = max_k |d_k| (pole guard as everywhere: |E - E_k| < 1e-10).
 //   2. Fixed-point operands (exact integers):  X'_ik = rint(w_ik d_k 2^{s_i}),  |X'| <= 2^54, with
-//      s_i from the bound max_k|w_ik| dmax;  W'_jk = rint(w_jk 2^{t_j}),  |W'| <= 2^52.
+//      s_i from the exact row maximum max_k|w_ik d_k|;  W'_jk = rint(w_jk 2^{t_j}),  |W'| <= 2^52.
 //      Then P_ij = sum_k X'_ik W'_jk is an exact integer, |P| <= nlev 2^106 < M/2 for nlev < 2^17,
 //      M = prod of the 16 pairwise-coprime moduli below (2^125.19).
 //   3. For each modulus m_l: V_l = X' mod m_l (uint8 in [0, m); balanced int8 when nlev > 65000),
@@ -14,7 +14,7 @@
 //   4. CRT (direct formula, exact 128-bit wrapping arithmetic) recovers P_ij in (-M/2, M/2); then
 //      R_ij = P_ij 2^{-s_i - t_j} / (2a), upper triangle mirrored (bitwise symmetric R).
 // The only approximation is the rounding of X and W to 55 / 53 significant bits relative to the row
-// bound (step 2): measured normwise error 3e-14 on darc rows (tools/ozaki_error.py), the level of an
+// maximum (step 2): measured normwise error 3e-14 on darc rows (tools/ozaki_error.py), the level of an
 // fp64 contraction; everything after it is exact integer arithmetic.
 #include <algorithm>
 #include <cstdio>
@@ -121,6 +121,38 @@ __global__ void __launch_bounds__(256) oz_rowmax_kernel(const double *__restrict
   }
 }
 
+// Exact row maxima xmax[e][i] = max_k |fl(w_ik d_k)| for the ne (<= 8) energies of a chunk: one CTA per
+// row, the w values read once for all energies. (A bound max|w_i.| * max|d| can overshoot by orders of
+// magnitude when the largest |d| sits on a pole with a small amplitude - the narrow resonances of
+// config fine - and the fixed-point rounding would then lose those bits.)
+__global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__ w, int64_t ldw, int nch, int nlev,
+                                                      int ne, const double *__restrict__ dbuf,
+                                                      double *__restrict__ xmax) {
+  const int i = blockIdx.x;
+  double mx[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) mx[e] = 0.0;
+  for (int k = threadIdx.x; k < nlev; k += blockDim.x) {
+    const double wv = w[static_cast<int64_t>(i) * ldw + k];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < ne) mx[e] = fmax(mx[e], fabs(wv * dbuf[static_cast<int64_t>(e) * nlev + k]));
+  }
+  __shared__ double red[8][8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx[e] = fmax(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], off));
+    if (lane_id() == 0) red[e][warp_id()] = mx[e];
+  }
+  __syncthreads();
+  if (threadIdx.x < ne) {
+    double m = 0.0;
+    for (int q = 0; q < 8; ++q) m = fmax(m, red[threadIdx.x][q]);
+    xmax[static_cast<int64_t>(threadIdx.x) * nch + i] = m;
+  }
+}
+
 // Fixed-point conversion + residues. One CTA per (row i, 2048-wide k chunk); each thread 8
 // consecutive k, its 8 w values loaded once and reused for all ne energies of the chunk.
 // dbuf == nullptr: the W operand (d = 1, BW bits, ne = 1); else the X operands of energies 0..ne-1.
@@ -132,7 +164,7 @@ __global__ void __launch_bounds__(256) oz_rowmax_kernel(const double *__restrict
 template <bool SIGNED>
 __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restrict__ w, int64_t ldw, int nch,
                                                          int nlev, int ne, const double *__restrict__ dbuf,
-                                                         const double *__restrict__ dmax,
+                                                         const double *__restrict__ xmax,
                                                          const double *__restrict__ rowmax, int bits,
                                                          int64_t ldv, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ shift) {
@@ -145,8 +177,8 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
   const int64_t plane = static_cast<int64_t>(nch) * ldv;
   const uint64_t bias = static_cast<uint64_t>(1) << BX;
   for (int e = 0; e < ne; ++e) {
-    // scale 2^s with bound * 2^s < 2^bits (bound = max|w_i.| * max|d|): frexp(bound) = f 2^ex, f < 1
-    const double bound = rowmax[i] * (dbuf ? dmax[e] : 1.0);
+    // scale 2^s with bound * 2^s < 2^bits (bound = the exact row maximum): frexp(bound) = f 2^ex, f < 1
+    const double bound = dbuf ? xmax[static_cast<int64_t>(e) * nch + i] : rowmax[i];
     int ex = 0;
     if (bound > 0.0 && isfinite(bound)) frexp(bound, &ex);
     const int s = bits - ex;
@@ -492,7 +524,7 @@ size_t rint8_ws_bytes(int64_t nch, int64_t nlev, int64_t ne) {
   b += static_cast<size_t>(i8::L) * nch * ldv;                       // U planes
   b += 2 * static_cast<size_t>(ne) * i8::L * nch * ldv;              // V planes (2 buffers)
   b += static_cast<size_t>(ne) * i8::L * nch * ldr;                  // residue planes
-  b += 2 * sizeof(double) * (static_cast<size_t>(ne) * nlev + ne);   // d, dmax (2 buffers)
+  b += 2 * sizeof(double) * (static_cast<size_t>(ne) * nlev + ne + static_cast<size_t>(ne) * nch);  // d, dmax, xmax
   b += sizeof(double) * nch;                                         // rowmax
   b += 2 * sizeof(int32_t) * (static_cast<size_t>(ne) * nch + ne);   // shifts, pole flags (2 buffers)
   b += sizeof(int32_t) * nch + sizeof(int2) * 4096 + 32 * 1024;      // t_j, tile list, alignment slack
@@ -523,11 +555,12 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   };
   int8_t *U = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(i8::L) * nch * ldv));
   int8_t *V[2];
-  double *dbuf[2], *dmax[2];
+  double *dbuf[2], *dmax[2], *xmax[2];
   int32_t *sx[2], *pflag[2];
   for (int b = 0; b < 2; ++b) {
     V[b] = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(chunk) * i8::L * nch * ldv));
     dbuf[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk * nlev));
+    xmax[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk * nch));
     dmax[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk));
     sx[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk * nch));
     pflag[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk));
@@ -581,13 +614,16 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, ss.aux>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
                                                                       dmax[b], pflag[b], stc);
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
+    i8::oz_xmax_kernel<<<static_cast<unsigned>(nch), 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch),
+                                                                       static_cast<int>(nlev), static_cast<int>(n),
+                                                                       dbuf[b], xmax[b]);
     if (x_signed)
       i8::oz_convert_kernel<true><<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
-                                                         static_cast<int>(n), dbuf[b], dmax[b], rowmax, i8::BX, ldv,
+                                                         static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX, ldv,
                                                          V[b], sx[b]);
     else
       i8::oz_convert_kernel<false><<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
-                                                          static_cast<int>(n), dbuf[b], dmax[b], rowmax, i8::BX,
+                                                          static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX,
                                                           ldv, V[b], sx[b]);
     cudaEventRecord(ss.conv_done[b], ss.aux);
   };

@@ -274,7 +274,7 @@ static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double
                               &c->i8s.gemm_done[1]})
         cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     }
-    *nl = 2 + 4 * static_cast<int>((ne + chunk - 1) / chunk);
+    *nl = 2 + 5 * static_cast<int>((ne + chunk - 1) / chunk);
     cudaEvent_t ga = nullptr;
     auto mark = [&](bool begin) {  // events around each INT8 GEMM launch (instrumentation only)
       if (!c->timing) return;

@@ -123,3 +123,29 @@ def test_int8_many_poles_signed_residues(ctx):
     for p, x in enumerate(E):
         ref, _ = oracle.R(w, Ek, 12.0, x)
         assert nrel(R[p], ref) < 1e-12, (x, nrel(R[p], ref))
+
+
+def test_int8_fine_block(ctx):
+    """fine (nch 1200, nlev 30000; 200 narrow resonance poles |w| ~ 1e-3 inside the window, which the
+    row-bound fixed-point rounding must not wash out): INT8 R against sampled oracle entries and the
+    DMMA R on dumped energies, |T|^2 against the DMMA path."""
+    import torch
+    import paper_1403_5524_b200 as rmx
+    c = syn.make_case("fine")
+    E = c.E[200000:200000 + 296]
+    dump = [0, 5, 250]
+    F, G, Fp, Gp = syn.asymptotic(c.eps, E, c.a)
+    no = syn.n_open(c.eps, E)
+    out8 = ctx.sweep(c.w, c.Ek, c.a, E, F, G, Fp, Gp, no, batch=296, dump_idx=dump)
+    ctx64 = rmx.Context()
+    out64 = ctx64.sweep(c.w, c.Ek, c.a, E, F, G, Fp, Gp, no, batch=296, dump_idx=dump)
+    torch.cuda.synchronize()
+    assert int((out8["status"] != 0).sum()) == 0
+    rng = np.random.default_rng(1)
+    for d, l in enumerate(dump):
+        R8, R64 = out8["R"][d].cpu().numpy(), out64["R"][d].cpu().numpy()
+        assert nrel(R8, R64) < 1e-12, nrel(R8, R64)
+        ii, jj = rng.integers(0, c.nch, 40), rng.integers(0, c.nch, 40)
+        vals, st = oracle.R_entries(c.w, c.Ek, c.a, E[l], ii, jj)
+        assert np.max(np.abs(R8[ii, jj] - vals)) / np.max(np.abs(R8)) < 1e-12
+        assert nrel(out8["T2"][d].cpu().numpy(), out64["T2"][d].cpu().numpy()) < 1e-8
