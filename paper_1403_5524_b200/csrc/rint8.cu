@@ -125,32 +125,66 @@ __global__ void __launch_bounds__(256) oz_rowmax_kernel(const double *__restrict
 // row, the w values read once for all energies. (A bound max|w_i.| * max|d| can overshoot by orders of
 // magnitude when the largest |d| sits on a pole with a small amplitude - the narrow resonances of
 // config fine - and the fixed-point rounding would then lose those bits.)
+// One CTA per 16 rows; the |d| values of the chunk's energies are staged through shared memory in
+// k-tiles of 512 (they would otherwise be re-read from L2 for every row), each warp owns 2 rows. The
+// maxima are fp32 UPPER bounds (operands and products rounded up): within 2^-20 of the exact value,
+// which only decides the exponent of the scale.
+// The k range is split over gridDim.y CTAs whose partial maxima meet by atomicMax on the float bit
+// patterns (non-negative floats order like their bits; max is order-independent: deterministic).
+constexpr int XM_ROWS = 16, XM_KT = 512, XM_KSPLIT = 8;
 __global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__ w, int64_t ldw, int nch, int nlev,
                                                       int ne, const double *__restrict__ dbuf,
-                                                      double *__restrict__ xmax) {
-  const int i = blockIdx.x;
-  double mx[8];
+                                                      float *__restrict__ xmax) {
+  __shared__ float ds[8][XM_KT];
+  const int r0 = blockIdx.x * XM_ROWS + warp_id() * 2;
+  float mx[2][8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) mx[e] = 0.0;
-  for (int k = threadIdx.x; k < nlev; k += blockDim.x) {
-    const double wv = w[static_cast<int64_t>(i) * ldw + k];
+  for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      if (e < ne) mx[e] = fmax(mx[e], fabs(wv * dbuf[static_cast<int64_t>(e) * nlev + k]));
+    for (int e = 0; e < 8; ++e) mx[r][e] = 0.0f;
+  const int ntile = (nlev + XM_KT - 1) / XM_KT;
+  const int t0 = static_cast<int>((static_cast<int64_t>(ntile) * blockIdx.y) / gridDim.y);
+  const int t1 = static_cast<int>((static_cast<int64_t>(ntile) * (blockIdx.y + 1)) / gridDim.y);
+  for (int k0 = t0 * XM_KT; k0 < t1 * XM_KT; k0 += XM_KT) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < 8 * XM_KT; q += blockDim.x) {
+      const int e = q / XM_KT, kk = q % XM_KT;
+      ds[e][kk] = (e < ne && k0 + kk < nlev)
+                      ? __double2float_ru(fabs(dbuf[static_cast<int64_t>(e) * nlev + k0 + kk]))
+                      : 0.0f;
+    }
+    __syncthreads();
+    // all 2 x 16 w loads of this lane issued before any use (the loop is latency-bound otherwise)
+    float wv[2][XM_KT / 32];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = r0 + r;
+      const double *wr = w + static_cast<int64_t>(i) * ldw + k0;
+#pragma unroll
+      for (int q = 0; q < XM_KT / 32; ++q) {
+        const int kk = lane_id() + 32 * q;
+        wv[r][q] = (i < nch && k0 + kk < nlev) ? __double2float_ru(fabs(wr[kk])) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int q = 0; q < XM_KT / 32; ++q) {
+        const int kk = lane_id() + 32 * q;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx[r][e] = fmaxf(mx[r][e], __fmul_ru(wv[r][q], ds[e][kk]));
+      }
   }
-  __shared__ double red[8][8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
+  for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx[e] = fmax(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], off));
-    if (lane_id() == 0) red[e][warp_id()] = mx[e];
-  }
-  __syncthreads();
-  if (threadIdx.x < ne) {
-    double m = 0.0;
-    for (int q = 0; q < 8; ++q) m = fmax(m, red[threadIdx.x][q]);
-    xmax[static_cast<int64_t>(threadIdx.x) * nch + i] = m;
-  }
+    for (int e = 0; e < 8; ++e) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) mx[r][e] = fmaxf(mx[r][e], __shfl_xor_sync(0xffffffffu, mx[r][e], off));
+      const int i = r0 + r;
+      if (lane_id() == 0 && i < nch && e < ne)
+        atomicMax(reinterpret_cast<int *>(xmax + static_cast<int64_t>(e) * nch + i), __float_as_int(mx[r][e]));
+    }
 }
 
 // Fixed-point conversion + residues. One CTA per (row i, 2048-wide k chunk); each thread 8
@@ -164,7 +198,7 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__
 template <bool SIGNED>
 __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restrict__ w, int64_t ldw, int nch,
                                                          int nlev, int ne, const double *__restrict__ dbuf,
-                                                         const double *__restrict__ xmax,
+                                                         const float *__restrict__ xmax,
                                                          const double *__restrict__ rowmax, int bits,
                                                          int64_t ldv, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ shift) {
@@ -177,8 +211,8 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
   const int64_t plane = static_cast<int64_t>(nch) * ldv;
   const uint64_t bias = static_cast<uint64_t>(1) << BX;
   for (int e = 0; e < ne; ++e) {
-    // scale 2^s with bound * 2^s < 2^bits (bound = the exact row maximum): frexp(bound) = f 2^ex, f < 1
-    const double bound = dbuf ? xmax[static_cast<int64_t>(e) * nch + i] : rowmax[i];
+    // scale 2^s with bound * 2^s < 2^bits (bound = the row maximum, rounded up): frexp = f 2^ex, f < 1
+    const double bound = dbuf ? static_cast<double>(xmax[static_cast<int64_t>(e) * nch + i]) : rowmax[i];
     int ex = 0;
     if (bound > 0.0 && isfinite(bound)) frexp(bound, &ex);
     const int s = bits - ex;
@@ -555,12 +589,13 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   };
   int8_t *U = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(i8::L) * nch * ldv));
   int8_t *V[2];
-  double *dbuf[2], *dmax[2], *xmax[2];
+  double *dbuf[2], *dmax[2];
+  float *xmax[2];
   int32_t *sx[2], *pflag[2];
   for (int b = 0; b < 2; ++b) {
     V[b] = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(chunk) * i8::L * nch * ldv));
     dbuf[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk * nlev));
-    xmax[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk * nch));
+    xmax[b] = reinterpret_cast<float *>(carve(sizeof(float) * chunk * nch));
     dmax[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk));
     sx[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk * nch));
     pflag[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk));
@@ -614,7 +649,10 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, ss.aux>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
                                                                       dmax[b], pflag[b], stc);
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
-    i8::oz_xmax_kernel<<<static_cast<unsigned>(nch), 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch),
+    cudaMemsetAsync(xmax[b], 0, sizeof(float) * chunk * nch, ss.aux);
+    i8::oz_xmax_kernel<<<dim3(static_cast<unsigned>((nch + i8::XM_ROWS - 1) / i8::XM_ROWS), i8::XM_KSPLIT), 256, 0,
+                         ss.aux>>>(
+        w, ldw, static_cast<int>(nch),
                                                                        static_cast<int>(nlev), static_cast<int>(n),
                                                                        dbuf[b], xmax[b]);
     if (x_signed)
