@@ -247,9 +247,13 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t sv = u2[q] * mc.c36 + u1[q] * mc.c18 + u0[q] + mc.off;
-        int r = static_cast<int>(sv - (__umulhi(sv, mc.m36) >> 4) * m);
-        if (SIGNED) r -= (r > (m - 1) / 2) ? m : 0;
-        pk[q >> 2] |= (static_cast<uint32_t>(r) & 0xFFu) << (8 * (q & 3));
+        const uint32_t r = sv - (__umulhi(sv, mc.m36) >> 4) * m;  // in [0, m)
+        if (SIGNED) {
+          const int rb = static_cast<int>(r) - ((static_cast<int>(r) > (m - 1) / 2) ? m : 0);
+          pk[q >> 2] |= (static_cast<uint32_t>(rb) & 0xFFu) << (8 * (q & 3));
+        } else {
+          pk[q >> 2] += r << (8 * (q & 3));  // r < 256: the bytes do not overlap
+        }
       }
       *reinterpret_cast<uint2 *>(o + l * plane) = make_uint2(pk[0], pk[1]);
     }
