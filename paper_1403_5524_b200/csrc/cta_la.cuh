@@ -80,6 +80,10 @@ __device__ __forceinline__ int tiles_in_row(int tm, int tiles_n, bool lower) {
 }
 
 __device__ __forceinline__ uint32_t round16(int bytes) { return static_cast<uint32_t>((bytes + 15) & ~15); }
+// first k slice of output tile (tm, tn) under the kband rule of GemmArgs
+__device__ __forceinline__ int kc_first(int kband, int tm, int tn) {
+  return kband == 1 ? (tm * BM) / BK : (kband == 2 ? (tn * BN) / BK : 0);
+}
 __device__ __forceinline__ int frag_perm(int g) { return (g >> 1) + 4 * (g & 1); }
 
 // Producer-warp helper: bulk-copy `nrows` rows of `rbytes` bytes (16-byte multiple) from
@@ -98,6 +102,10 @@ struct GemmArgs {
   bool lower, read_c;  // read_c: C -= A.B (C must be 16-byte aligned, ldc even); else C = A.B + diag_add I
   bool trans_c;        // store the result transposed (only with read_c == false)
   double diag_add;
+  // leading k range known to contribute zero (triangular operands): 0 none; 1 A(i, k) = 0 for
+  // k < i (k starts at the output tile's first row); 2 B(j, k) = 0 for k < j (k starts at the
+  // output tile's first column). Whole BK slices are skipped; the rest must hold explicit zeros.
+  int kband;
 };
 
 // C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).
@@ -160,7 +168,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
         bulk_rows(Cs, CS_LD, ga.C + static_cast<int64_t>(tm * BM) * ga.ldc + tn * BN, ga.ldc, rows,
                   rb, &gs->cfull);
       }
-      for (int kc = 0; kc < nkc; ++kc, ++it) {
+      for (int kc = kc_first(ga.kband, tm, tn); kc < nkc; ++kc, ++it) {
         const int st = it % STAGES, use = it / STAGES;
         if (it >= STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
         if (lane == 0) {
@@ -261,7 +269,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
-      for (int kc = 0; kc < nkc; ++kc, ++it) {
+      for (int kc = kc_first(ga.kband, tm, tn); kc < nkc; ++kc, ++it) {
         const int st = it % STAGES, use = it / STAGES;
         mbar_wait(&gs->full[st], use & 1);
         const int krem = min(BK, K - kc * BK);
@@ -368,6 +376,13 @@ __device__ __forceinline__ void gemm_sub(int M, int N, int K, const Op &a, const
                                          const MatView &c, int cr0, int cc0, bool lower,
                                          double *smem, GemmSync *gs) {
   GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, true, false, 0.0};
+  gemm_rt(ga, gemm_smem_align(smem), gs);
+}
+// C = A.B with a known-zero leading k band (GemmArgs::kband)
+__device__ __forceinline__ void gemm_set_kb(int M, int N, int K, const Op &a, const Op &b,
+                                            const MatView &c, int cr0, int cc0, bool lower, int kband,
+                                            double *smem, GemmSync *gs) {
+  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, false, 0.0, kband};
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 // C = A.B + diag_add I

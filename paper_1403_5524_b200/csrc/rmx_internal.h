@@ -22,7 +22,7 @@ struct MatchLayout {
   int64_t npad, ldm, m_off, tg_off, slot;
 };
 struct TepiLayout {
-  int64_t ldo, s_off, x_off, k_off, tg_off, slot;
+  int64_t ldo, s_off, x_off, k_off, tg_off, tt_off, slot;
 };
 __host__ __device__ inline MatchLayout match_layout(int64_t nch) {
   MatchLayout L;
@@ -40,7 +40,8 @@ __host__ __device__ inline TepiLayout tepi_layout(int64_t nch) {
   L.x_off = nch * L.ldo + 32;
   L.k_off = L.x_off + nch * L.ldo + 32;
   L.tg_off = L.k_off + nch * L.ldo + 32;
-  L.slot = L.tg_off + 128 * 128 + 32;
+  L.tt_off = L.tg_off + 128 * 128 + 32;  // 128 x ldo scratch of the triangular inverse
+  L.slot = L.tt_off + 128 * L.ldo + 32;
   return L;
 }
 

@@ -65,11 +65,12 @@ __global__ void __launch_bounds__(NT, 1)
   const TepiLayout L = tepi_layout(n);
   const int ldo = static_cast<int>(L.ldo);
   double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
-  const CUtensorMap *vw = views + blockIdx.x * 4 * NVIEW;
+  const CUtensorMap *vw = views + blockIdx.x * 5 * NVIEW;
   const MatView Sv{vw + 0 * NVIEW, slot + L.s_off, ldo};
   const MatView Xv{vw + 1 * NVIEW, slot + L.x_off, ldo};
   const MatView Kv{vw + 2 * NVIEW, slot + L.k_off, ldo};
   const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, TG};
+  const MatView Ttv{vw + 4 * NVIEW, slot + L.tt_off, ldo};
   double *S = Sv.base;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
@@ -85,7 +86,8 @@ __global__ void __launch_bounds__(NT, 1)
     }
     int bad = 0;
     if (o > 0) {
-      // Kc = X = K_oo (aligned, even pitch: operands of the TMA GEMM pipeline)
+      // Kc = K_oo (aligned, even pitch: operand of the TMA GEMM pipeline); X = 0 (Z = L^{-1} is
+      // built there, its strict upper part must stay zero)
       for (int i = warp_id(); i < o; i += NW) {
         const double *src = Ke + static_cast<int64_t>(i) * ldk;
         double *dk = Kv.at(i, 0), *dx = Xv.at(i, 0);
@@ -98,13 +100,13 @@ __global__ void __launch_bounds__(NT, 1)
           for (int q = 0; q < U; ++q)
             if (j0 + 32 * q < o) {
               dk[j0 + 32 * q] = v[q];
-              dx[j0 + 32 * q] = v[q];
+              dx[j0 + 32 * q] = 0.0;
             }
         }
       }
       if (pa.g) {
-        // NEXT-1 (10): v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) into X column o (the extra
-        // right-hand side of the solves below); gG_i staged in shared memory, i ascending
+        // NEXT-1 (10): v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) into Kc column o; gG_i staged in
+        // shared memory, i ascending
         const double *ge = pa.g + e * n, *Fpe = pa.Fp + e * n, *Gpe = pa.Gp + e * n;
         double *gG = sm.gemm;
         for (int i = threadIdx.x; i < n; i += NT) gG[i] = ge[i] * Gpe[i];
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(NT, 1)
         for (int j = threadIdx.x; j < o; j += NT) {
           double s = ge[j] * Fpe[j];
           for (int i = 0; i < n; ++i) s = fma(gG[i], Ke[static_cast<int64_t>(i) * ldk + j], s);
-          *Xv.at(j, o) = 0.5 * s;
+          *Kv.at(j, o) = 0.5 * s;
         }
       }
       __syncthreads();
@@ -133,27 +135,50 @@ __global__ void __launch_bounds__(NT, 1)
                    smg, gs);
         }
       }
-      // forward: L Z = K  (X holds K_oo [| v]); X_p = L_pp^{-1} X_p (in place, one 128-row tile row)
-      const int nr = o + (pa.g ? 1 : 0);  // right-hand sides
-      for (int P0 = 0; P0 < o; P0 += NB) {
-        const int W = min(NB, o - P0);
-        tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
-        gemm_set(W, nr, W, opk(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
-        if (P0 + W < o)
-          gemm_sub(o - P0 - W, nr, W, opk(Sv, P0 + W, P0), opn(Xv, P0, 0), Xv, P0 + W, 0, false, smg, gs);
+      // Z = L^{-1} (lower, in X) block row by block row:  Z_bb = L_bb^{-1} (128 x 128 inverse),
+      // Z_{b,0:b} = -Z_bb (L_{b,0:b} Z_{0:b,0:b}); the triangular factor Z of the product skips its
+      // zero k slices (kband 2), so the step costs (1/3) o^3 in total
+      for (int R0 = 0; R0 < o; R0 += NB) {
+        const int W = min(NB, o - R0);
+        tri_inv128(Sv, R0, W, TRI_LOWER, Tv, smg, gs);
+        if (R0 > 0) {
+          gemm_set_kb(W, R0, R0, opk(Sv, R0, 0), opn(Xv, 0, 0), Ttv, 0, 0, false, 2, smg, gs);
+          gemm_sub(W, R0, W, opk(Tv, 0, 0), opn(Ttv, 0, 0), Xv, R0, 0, false, smg, gs);
+        }
+        for (int q = threadIdx.x; q < W * W; q += NT) {
+          const int r = q / W, cc = q % W;
+          *Xv.at(R0 + r, R0 + cc) = Tv.base[r * TG + cc];  // upper part of Tv is zero
+        }
+        __syncthreads();
       }
-      // backward: L^T X = Z; X_p = L_pp^{-T} X_p: A(i, k) = Tg[k][i]
-      for (int P0 = ((o - 1) / NB) * NB; P0 >= 0; P0 -= NB) {
-        const int W = min(NB, o - P0);
-        tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
-        gemm_set(W, nr, W, opn(Tv, 0, 0), opn(Xv, P0, 0), Xv, P0, 0, false, 0.0, smg, gs);
-        if (P0 > 0)
-          // X[0:P0] -= (L[P0:P0+W, 0:P0])^T X[P0:P0+W]
-          gemm_sub(P0, nr, W, opn(Sv, P0, 0), opn(Xv, P0, 0), Xv, 0, 0, false, smg, gs);
-      }
-      // P = K_oo X = K S^{-1} K is symmetric: lower tiles only (half the flops), then mirrored
-      gemm_set(o, o, o, opk(Kv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, true, 0.0, smg, gs);
+      // S^{-1} = Z^T Z (lower tiles, kband 1: Z(k, i) = 0 for k < i), over L, then mirrored
+      gemm_set_kb(o, o, o, opn(Xv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, true, 1, smg, gs);
       mirror_lower(S, ldo, o, sm.gemm);
+      // X = S^{-1} K_oo = (I + K^2)^{-1} K: symmetric (K_oo symmetric, reading M1), lower tiles then
+      // mirrored; overwrites Z
+      gemm_set(o, o, o, opk(Sv, 0, 0), opn(Kv, 0, 0), Xv, 0, 0, true, 0.0, smg, gs);
+      mirror_lower(Xv.base, ldo, o, sm.gemm);
+      if (pa.g) {
+        // NEXT-1 (11): y = S^{-1} v into X column o (v in Kc column o)
+        double *vs = sm.gemm;
+        for (int j = threadIdx.x; j < o; j += NT) vs[j] = *Kv.at(j, o);
+        __syncthreads();
+        for (int i = warp_id(); i < o; i += NW) {
+          const double *sr = Sv.at(i, 0);
+          double t = 0.0;
+          for (int j = lane_id(); j < o; j += 32) t = fma(sr[j], vs[j], t);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+          if (lane_id() == 0) *Xv.at(i, o) = t;
+        }
+      }
+      // P = K_oo X = K S^{-1} K = I - S^{-1} (K and S commute): in place of S^{-1}
+      __syncthreads();
+      for (int i = warp_id(); i < o; i += NW) {
+        double *pr = Sv.at(i, 0);
+        for (int j = lane_id(); j < o; j += 32) pr[j] = (i == j ? 1.0 : 0.0) - pr[j];
+      }
+      __syncthreads();
     }
     // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
@@ -243,11 +268,12 @@ __global__ void __launch_bounds__(NT, 1)
 
 int64_t tepi_ws_doubles_per_slot(int64_t nch) { return tepi_layout(nch).slot; }
 
-// Matrices of one slot whose TMA descriptors the kernel uses: (S, X, Kc, Tg), NVIEW boxes each.
+// Matrices of one slot whose TMA descriptors the kernel uses: (S, X, Kc, Tg, Tt), NVIEW boxes each.
 void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
   const TepiLayout L = tepi_layout(nch);
   specs = {MatSpec{L.s_off, nch, L.ldo, L.ldo}, MatSpec{L.x_off, nch, L.ldo, L.ldo},
-           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, TG, TG, TG}};
+           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, TG, TG, TG},
+           MatSpec{L.tt_off, NB, L.ldo, L.ldo}};
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
