@@ -44,6 +44,8 @@ struct ModConst {
   float inv;          // 1/m (rounded down a little: q never overestimates by more than 1)
   uint32_t magic;     // ceil(2^32 / m): umulhi(s, magic) is floor(s/m) or one more for s < 2^28
   uint32_t m36;       // ceil(2^36 / m): umulhi(s, m36) >> 4 == floor(s/m) exactly for s < 2^28, m < 256
+  uint32_t blo, bhi;  // byte weights (2^{8b} mod m, b = 0..3 | 4..7) packed for dp4a
+  uint32_t boff;      // (-2^BX) mod m: removes the bias of u = X' + 2^BX
 };
 __constant__ ModConst c_mod[L];
 
@@ -193,8 +195,8 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__
 // out: planes [ne][L][nch][ldv] int8 (ldv multiple of 16); shift: [ne][nch] exponents s_i / t_j.
 // SIGNED: balanced residues in [-(m-1)/2, (m-1)/2] (int8; needed when nlev > 65000), else plain
 // residues in [0, m) (uint8 operand: u8 x s8 products stay < 2^31 summed over nlev <= 65000).
-// Per residue: s = u2 c36 + u1 c18 + u0 + off (< 2^28), q = umulhi(s, ceil(2^36/m)) >> 4 (exact),
-// r = s - q m. The modulus 256 residue is the low byte of the two's-complement value.
+// Per residue: s = sum_b byte_b(u) (2^{8b} mod m) + (-2^54 mod m) (< 2^19, two dp4a),
+// q = umulhi(s, ceil(2^32/m)) (exact), r = s - q m. The modulus 256 residue is the low byte of the two's-complement value.
 template <bool SIGNED>
 __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restrict__ w, int64_t ldw, int nch,
                                                          int nlev, int ne, const double *__restrict__ dbuf,
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
     if (blockIdx.x == 0 && threadIdx.x == 0) shift[static_cast<int64_t>(e) * nch + i] = s;
     if (k0 >= nlev) continue;
     const double *dr = dbuf ? dbuf + static_cast<int64_t>(e) * nlev + k0 : nullptr;
-    uint32_t u2[8], u1[8], u0[8];
+    uint32_t uh[8], ul[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       double x = wv[q];
@@ -228,15 +230,14 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
       x *= scale;
       if (!isfinite(x)) x = 0.0;  // pole energies: R is NaN anyway (status POLE)
       const uint64_t u = static_cast<uint64_t>(__double2ll_rn(x) + static_cast<long long>(bias));
-      u2[q] = static_cast<uint32_t>(u >> 36);
-      u1[q] = static_cast<uint32_t>((u >> 18) & 0x3FFFF);
-      u0[q] = static_cast<uint32_t>(u & 0x3FFFF);
+      uh[q] = static_cast<uint32_t>(u >> 32);
+      ul[q] = static_cast<uint32_t>(u);
     }
     int8_t *o = out + static_cast<int64_t>(e) * L * plane + static_cast<int64_t>(i) * ldv + k0;
     {  // modulus 256: the low byte (u = X' + 2^54, 2^54 = 0 mod 256)
       uint32_t pk[2] = {0u, 0u};
 #pragma unroll
-      for (int q = 0; q < 8; ++q) pk[q >> 2] |= (u0[q] & 0xFFu) << (8 * (q & 3));
+      for (int q = 0; q < 8; ++q) pk[q >> 2] |= (ul[q] & 0xFFu) << (8 * (q & 3));
       *reinterpret_cast<uint2 *>(o) = make_uint2(pk[0], pk[1]);
     }
 #pragma unroll
@@ -246,8 +247,10 @@ __global__ void __launch_bounds__(256) oz_convert_kernel(const double *__restric
       uint32_t pk[2] = {0u, 0u};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint32_t sv = u2[q] * mc.c36 + u1[q] * mc.c18 + u0[q] + mc.off;
-        const uint32_t r = sv - (__umulhi(sv, mc.m36) >> 4) * m;  // in [0, m)
+        // sv = sum_b byte_b(u) (2^{8b} mod m) + (-2^BX mod m) < 7 * 255^2 + 256 < 2^19 (two dp4a), so
+        // q = umulhi(sv, ceil(2^32/m)) is floor(sv/m) exactly (error sv/2^32 < 2^-13 < 1/m)
+        const uint32_t sv = __dp4a(uh[q], mc.bhi, __dp4a(ul[q], mc.blo, mc.boff));
+        const uint32_t r = sv - __umulhi(sv, mc.magic) * m;  // in [0, m)
         if (SIGNED) {
           const int rb = static_cast<int>(r) - ((static_cast<int>(r) > (m - 1) / 2) ? m : 0);
           pk[q >> 2] |= (static_cast<uint32_t>(rb) & 0xFFu) << (8 * (q & 3));
@@ -503,6 +506,12 @@ static cudaError_t init_i8_consts() {
     mc[l].inv = nextafterf(1.0f / static_cast<float>(m), 0.0f);
     mc[l].magic = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 32) + m - 1) / m);
     mc[l].m36 = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 36) + m - 1) / m);
+    mc[l].blo = mc[l].bhi = 0;
+    for (int b = 0; b < 4; ++b) {
+      mc[l].blo |= static_cast<uint32_t>((static_cast<uint64_t>(1) << (8 * b)) % m) << (8 * b);
+      mc[l].bhi |= static_cast<uint32_t>((static_cast<uint64_t>(1) << (8 * b + 32)) % m) << (8 * b);
+    }
+    mc[l].boff = static_cast<uint32_t>((m - p54) % m);
     // C_l = (M/m) * ((M/m)^-1 mod m)
     const unsigned __int128 Ml = M / static_cast<unsigned>(m);
     const int Mlm = static_cast<int>(Ml % static_cast<unsigned>(m));
