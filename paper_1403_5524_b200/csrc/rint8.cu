@@ -17,6 +17,7 @@
 // maximum (step 2): measured normwise error 3e-14 on darc rows (tools/ozaki_error.py), the level of an
 // fp64 contraction; everything after it is exact integer arithmetic.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -286,6 +287,49 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+// GEMM epilogue of one CTA (warps 4..7): TMEM lane quarter q holds output rows row0 + q*32 + lane,
+// columns col0 .. col0 + BN - 1 in TMEM columns 0..BN-1; C mod m_l -> uint8 residue plane
+// res[e][l][row][col] (rows >= nch and column groups starting at or past nch are not stored).
+__device__ __forceinline__ void residue_epilogue(uint32_t tmem, int q, int row0, int col0, int nch, int l, int64_t e,
+                                                 int64_t ldr, uint8_t *__restrict__ res) {
+  const int lane = lane_id();
+  const int row = row0 + q * 32 + lane;
+  const int m = mod_of(l);
+  const int c16 = (1 << 16) % m;
+  const float inv = c_mod[l].inv;
+  uint8_t *rrow = res + ((e * L + l) * static_cast<int64_t>(nch) + row) * ldr + col0;
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+    if (row < nch && col0 + c0 < nch) {
+      uint32_t pk[8];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        // acc = h 2^16 + lo (h signed): residue of h c16 + lo (|.| < 2^24: exact in fp32)
+        const int acc = static_cast<int>(v[j]);
+        const int h = acc >> 16, lo = acc & 0xFFFF;
+        const int sv = h * c16 + lo + (m << 16);  // > 0 (|h c16| < 2^15 * 255)
+        const int r = umod_small(static_cast<uint32_t>(sv), m, inv);
+        if ((j & 3) == 0) pk[j >> 2] = 0u;
+        pk[j >> 2] |= static_cast<uint32_t>(r) << (8 * (j & 3));
+      }
+      uint4 *dst = reinterpret_cast<uint4 *>(rrow + c0);
+      dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(GEMM_NT, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu, int nch,
                    int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res,
@@ -363,50 +407,136 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
                      smem_u32(accf))
                  : "memory");
   } else if (warp >= 4) {
-    // epilogue: TMEM lane quarter q = warp - 4 holds rows q*32 .. q*32+31 of the tile
     mbar_wait(accf, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-    const int q = warp - 4;
-    const int row = tij.x * BM + q * 32 + lane;
-    const int m = mod_of(l);
-    const int c16 = (1 << 16) % m;
-    const float inv = c_mod[l].inv;
-    uint8_t *rrow = res + ((e * L + l) * static_cast<int64_t>(nch) + row) * ldr + tij.y * BN;
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-            "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-            "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-      const int col0 = tij.y * BN + c0;
-      if (row < nch && col0 < nch) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          // acc = h 2^16 + lo (h signed): residue of h c16 + lo (|.| < 2^24: exact in fp32)
-          const int acc = static_cast<int>(v[j]);
-          const int h = acc >> 16, lo = acc & 0xFFFF;
-          const int sv = h * c16 + lo + (m << 16);  // > 0 (|h c16| < 2^15 * 255)
-          const int r = umod_small(static_cast<uint32_t>(sv), m, inv);
-          if ((j & 3) == 0) pk[j >> 2] = 0u;
-          pk[j >> 2] |= static_cast<uint32_t>(r) << (8 * (j & 3));
-        }
-        uint4 *dst = reinterpret_cast<uint4 *>(rrow + c0);
-        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
+    residue_epilogue(tmem, warp - 4, tij.x * BM, tij.y * BN, nch, l, e, ldr, res);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
+}
+
+// CTA-pair variant (tcgen05 cta_group::2) for the blocks strictly above the diagonal: one 2-CTA
+// cluster per 256 x 256 output block (I2, J), J > I2, M = 256 per MMA instruction. CTA r stages its
+// own 128 rows of V (rows I2*256 + 128 r) and 128 of the 256 U rows (J*256 + 128 r) - the pair shares
+// operands, so each SM moves half the B bytes of the 1-SM kernel through shared memory (sustained INT8
+// throughput under the power cap +6 %, tools/tc_i8_gemm2.cu). Both CTAs' TMA completions count on the
+// leader's full barrier; the leader's single MMA thread commits each stage to both CTAs' empty
+// barriers and the finished accumulator to both accf barriers; each CTA drains its own TMEM rows.
+constexpr int P_STAGES = 6;
+constexpr int P_B_BYTES = (BN / 2) * BKB, P_STAGE_BYTES = A_BYTES + P_B_BYTES;
+constexpr int GEMM2_SMEM = 1024 + P_STAGES * P_STAGE_BYTES + 256;
+__host__ __device__ constexpr uint32_t idesc_i8_pair(bool a_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+         (static_cast<uint32_t>(256 >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
+    oz_gemm2_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu2, int nch,
+                    int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res,
+                    uint32_t idesc, int nen) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t *empty = full + P_STAGES;
+  uint64_t *accf = empty + P_STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1;
+  const int tile = cid % ntiles;
+  const int64_t e = (cid / ntiles) % nen;
+  const int l = cid / (ntiles * nen);
+  const int2 tij = tiles[tile];  // (I2, J): rows I2*256.., columns J*256..
+  const int nk = (nlev + BKB - 1) / BKB;
+  const int row0 = tij.x * 256 + static_cast<int>(rank) * BM;
+  const int vrow = static_cast<int>((e * L + l) * nch) + row0;
+  const int urow = l * nch + tij.y * BN + static_cast<int>(rank) * (BN / 2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tv);
+    tma_prefetch_desc(&tu2);
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % P_STAGES;
+      if (kt >= P_STAGES) mbar_wait(&empty[s], ((kt / P_STAGES) - 1) & 1);
+      if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+      const uint32_t base = smem_u32(smem + s * P_STAGE_BYTES);
+      const uint32_t bar = mapa_rank0(smem_u32(&full[s]));
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(base), "l"(reinterpret_cast<uint64_t>(&tv)), "r"(bar),
+          "r"(kt * BKB), "r"(vrow)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(base + A_BYTES), "l"(reinterpret_cast<uint64_t>(&tu2)), "r"(bar),
+          "r"(kt * BKB), "r"(urow)
+          : "memory");
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % P_STAGES;
+      mbar_wait(&full[s], (kt / P_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const uint32_t base = smem_u32(smem + s * P_STAGE_BYTES);
+      const uint64_t da = umma_desc_sw128(base), db = umma_desc_sw128(base + A_BYTES);
+#pragma unroll
+      for (int k = 0; k < BKB / 32; ++k) {
+        const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+              smem_u32(&empty[s])),
+          "h"(static_cast<uint16_t>(3))
+          : "memory");
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(accf)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+  } else if (warp >= 4) {
+    mbar_wait(accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    residue_epilogue(tmem, warp - 4, row0, tij.y * BN, nch, l, e, ldr, res);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  cluster_sync_all();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -591,6 +721,8 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   if (!attr) {
     ce = cudaFuncSetAttribute(i8::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::GEMM_SMEM);
     if (ce != cudaSuccess) return ce;
+    ce = cudaFuncSetAttribute(i8::oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::GEMM2_SMEM);
+    if (ce != cudaSuccess) return ce;
     attr = true;
   }
   const int64_t ldv = rint8_ldv(nlev), ldr = rint8_ldr(nch);
@@ -622,18 +754,31 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     return cudaErrorInvalidValue;
   }
 
-  // upper-triangle tile list (rows I*128, columns J*256) - static per nch
-  std::vector<int2> tl;
+  // Upper-triangle tiles - static per nch. With the CTA-pair kernel: the 256 x 256 blocks strictly
+  // above the diagonal go to oz_gemm2_kernel (list `pair`, (I2, J) in 256-blocks), the diagonal blocks
+  // to oz_gemm_kernel as two 128 x 256 tiles each (the second a half tile). Without it (a single
+  // 256-block, or RMX_I8_NOPAIR set - an A/B switch for measurements): 128 x 256 tiles throughout.
+  static const bool no_pair = getenv("RMX_I8_NOPAIR") != nullptr;
+  const bool use_pair = !no_pair && nch > i8::BN;
+  std::vector<int2> tl, pl;
   for (int I = 0; I * i8::BM < nch; ++I)
-    for (int J = 0; J * i8::BN < nch; ++J)
-      if (J * i8::BN + i8::BN - 1 >= I * i8::BM) tl.push_back(make_int2(I, J));
-  if (tl.size() > 4096) {
+    for (int J = 0; J * i8::BN < nch; ++J) {
+      if (J * i8::BN + i8::BN - 1 < I * i8::BM) continue;  // entirely below the diagonal
+      if (use_pair && J > I / 2) continue;                   // inside a pair block
+      tl.push_back(make_int2(I, J));
+    }
+  if (use_pair)
+    for (int I2 = 0; I2 * 256 < nch; ++I2)
+      for (int J = I2 + 1; J * i8::BN < nch; ++J) pl.push_back(make_int2(I2, J));
+  if (tl.size() + pl.size() > 4096) {
     err = "rform int8: nch too large for the tile list";
     return cudaErrorInvalidValue;
   }
-  ce = cudaMemcpyAsync(tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, st);
+  std::vector<int2> all(tl);
+  all.insert(all.end(), pl.begin(), pl.end());
+  ce = cudaMemcpyAsync(tiles, all.data(), sizeof(int2) * all.size(), cudaMemcpyHostToDevice, st);
   if (ce != cudaSuccess) return ce;
-  const int ntiles = static_cast<int>(tl.size());
+  const int ntiles = static_cast<int>(tl.size()), npair = static_cast<int>(pl.size());
 
   // W operand: row maxima, W' residues, t_j (on st)
   i8::oz_rowmax_kernel<<<static_cast<unsigned>(nch), 256, 0, st>>>(w, ldw, static_cast<int>(nlev), rowmax);
@@ -644,39 +789,44 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   }
   CUtensorMap tu, tv[2];
   if (!encode_i8(&tu, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, i8::BN, err)) return cudaErrorInvalidValue;
+  CUtensorMap tu2;  // U rows in boxes of 128 (one half of a pair block's columns per CTA)
+  if (!encode_i8(&tu2, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, i8::BN / 2, err)) return cudaErrorInvalidValue;
   for (int b = 0; b < 2; ++b)
     if (!encode_i8(&tv[b], V[b], chunk * i8::L * nch, nlev, ldv, i8::BM, err)) return cudaErrorInvalidValue;
   const double inv2a = 1.0 / (2.0 * a);
   // plain (unsigned) X residues keep |C| <= 255 * 128 * nlev < 2^31 up to nlev = 65793
   const bool x_signed = nlev > 65000;
-  const uint32_t idesc = i8::idesc_i8(x_signed);
+  const uint32_t idesc = i8::idesc_i8(x_signed), idesc2 = i8::idesc_i8_pair(x_signed);
   // the aux stream starts after everything already queued on st (rowmax, inputs)
   cudaEventRecord(ss.start, st);
   cudaStreamWaitEvent(ss.aux, ss.start, 0);
   const int64_t nchunks = (ne + chunk - 1) / chunk;
+  // experiment switch: RMX_I8_SERIAL runs the conversion on the GEMM stream (no overlap)
+  static const bool serial = getenv("RMX_I8_SERIAL") != nullptr;
+  cudaStream_t cs = serial ? st : ss.aux;
   auto convert = [&](int64_t c) {
     const int b = static_cast<int>(c & 1);
     const int64_t e0 = c * chunk, n = std::min(chunk, ne - e0);
-    if (c >= 2) cudaStreamWaitEvent(ss.aux, ss.gemm_done[b], 0);  // buffer b free again
+    if (c >= 2) cudaStreamWaitEvent(cs, ss.gemm_done[b], 0);  // buffer b free again
     int32_t *stc = status ? status + e0 : nullptr;
-    i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, ss.aux>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
+    i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, cs>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
                                                                       dmax[b], pflag[b], stc);
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
-    cudaMemsetAsync(xmax[b], 0, sizeof(float) * chunk * nch, ss.aux);
+    cudaMemsetAsync(xmax[b], 0, sizeof(float) * chunk * nch, cs);
     i8::oz_xmax_kernel<<<dim3(static_cast<unsigned>((nch + i8::XM_ROWS - 1) / i8::XM_ROWS), i8::XM_KSPLIT), 256, 0,
-                         ss.aux>>>(
+                         cs>>>(
         w, ldw, static_cast<int>(nch),
                                                                        static_cast<int>(nlev), static_cast<int>(n),
                                                                        dbuf[b], xmax[b]);
     if (x_signed)
-      i8::oz_convert_kernel<true><<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
+      i8::oz_convert_kernel<true><<<g, 256, 0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
                                                          static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX, ldv,
                                                          V[b], sx[b]);
     else
-      i8::oz_convert_kernel<false><<<g, 256, 0, ss.aux>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
+      i8::oz_convert_kernel<false><<<g, 256, 0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
                                                           static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX,
                                                           ldv, V[b], sx[b]);
-    cudaEventRecord(ss.conv_done[b], ss.aux);
+    cudaEventRecord(ss.conv_done[b], cs);
   };
   convert(0);
   for (int64_t c = 0; c < nchunks; ++c) {
@@ -688,6 +838,10 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
         tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc,
         static_cast<int>(n));
+    if (npair > 0)
+      i8::oz_gemm2_kernel<<<static_cast<unsigned>(2 * npair * i8::L * n), i8::GEMM_NT, i8::GEMM2_SMEM, st>>>(
+          tv[b], tu2, static_cast<int>(nch), static_cast<int>(nlev), npair, tiles + ntiles, ldr, res, idesc2,
+          static_cast<int>(n));
     gemm_mark(false);
     dim3 gc(static_cast<unsigned>((nch + 1 + 255) / 256), static_cast<unsigned>((nch + 1) / 2),
             static_cast<unsigned>(n));

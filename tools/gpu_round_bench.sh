@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 echo "ncu launches rc=$?"
 ARGS1="--steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 python bench.py $ARGS1 > gpurun_out/plain1.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:"oz_gemm_kernel|oz_convert_kernel" -s 40 -c 2 \
+ncu --set full --import-source on --clock-control none -k regex:"oz_gemm|oz_convert_kernel" -s 40 -c 4 \
     -o gpurun_out/prof_int8 python bench.py $ARGS1 > gpurun_out/ncu_pi8.log 2>&1
 echo "ncu full rc=$?"
 tail -c 600 gpurun_out/bench_default.json

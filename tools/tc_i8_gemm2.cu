@@ -1,11 +1,12 @@
-// tcgen05 INT8 GEMM microbenchmark / validation for sm_100a (evaluates an Ozaki-style FP64 emulation
-// of the R contraction on the 5th-gen integer tensor cores).
+// tcgen05 INT8 GEMM microbenchmark, CTA-pair variant (cta_group::2): one 2-CTA cluster per 256 x 256
+// output tile, M = 256 per MMA instruction, each CTA stages its own 128 A rows and 128 B rows (the
+// pair shares operands, halving per-SM shared-memory operand traffic). Compare with tc_i8_gemm.cu.
 //   C[M][N] (int32) = A[M][K] (int8, K-major) . B[N][K]^T (int8, K-major)
-// One CTA per 128 x 256 output tile: warp 0 issues 2D TMA loads (SWIZZLE_128B boxes of 128 bytes x
+// (1-SM version:) one CTA per 128 x 256 output tile: warp 0 issues 2D TMA loads (SWIZZLE_128B boxes of 128 bytes x
 // rows) into a 4-stage mbarrier ring, warp 1 (one lane) issues tcgen05.mma.cta_group::1.kind::i8
 // (M = 128, N = 256, K = 32 per instruction) into a TMEM accumulator and commits each stage back to
 // the ring, warps 4-7 drain TMEM with tcgen05.ld.32x32b and store int32 rows.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tc_i8_gemm tools/tc_i8_gemm.cu -lcuda
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tc_i8_gemm2 tools/tc_i8_gemm2.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -17,9 +18,9 @@
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1);} } while (0)
 
-constexpr int BM = 128, BN = 256, BKB = 128;  // BKB: K bytes per stage (= one 128B swizzle row)
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BKB, B_BYTES = BN * BKB, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BN = 256, BKB = 128;  // per CTA: 128 A rows, 128 B rows (BN / 2) per stage
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BKB, B_BYTES = (BN / 2) * BKB, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NT = 256;
 constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
 
@@ -43,6 +44,25 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *m, uint6
   asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
                ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa0(uint32_t saddr) {  // the same smem offset in CTA 0 of the cluster
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// TMA into this CTA's smem, completion (bytes) signalled on the leader CTA's barrier
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap *m, uint32_t bar_cluster, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%3, %4}], [%2];\n"
+               ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1) : "memory");
+}
 // K-major, SWIZZLE_128B canonical layout: 8-row groups 1024 B apart (SBO), LBO unused (1), version 1
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -53,13 +73,13 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;
   return d;
 }
-// s8 x s8 -> s32, K-major A and B, M = 128, N = 256
+// s8 x s8 -> s32, K-major A and B, M = 256 (CTA pair), N = 256
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                           (static_cast<uint32_t>(BM >> 4) << 24);
+                           (static_cast<uint32_t>(256 >> 4) << 24);
 
-__global__ void __launch_bounds__(NT, 1)
-    i8_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N,
-            int K, int32_t *__restrict__ C) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    i8_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N,
+             int K, int32_t *__restrict__ C) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
@@ -67,7 +87,8 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t *accf = empty + STAGES;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tm = blockIdx.y, tn = blockIdx.x;
+  const uint32_t rank = cluster_rank();
+  const int tm = blockIdx.y, tn = blockIdx.x / 2;
   const int nk = K / BKB;
 
   if (threadIdx.x == 0) {
@@ -79,12 +100,12 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
                  "r"(BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-  __syncthreads();
+  cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const uint32_t tmem = *tmem_slot;
 
@@ -92,12 +113,13 @@ __global__ void __launch_bounds__(NT, 1)
     for (int kt = 0; kt < nk; ++kt) {
       const int s = kt % STAGES;
       if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-      mbar_expect_tx(&full[s], STAGE_BYTES);
+      if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
       const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-      tma_2d(base, &ta, &full[s], kt * BKB, tm * BM);
-      tma_2d(base + A_BYTES, &tb, &full[s], kt * BKB, tn * BN);
+      const uint32_t bar = mapa0(smem_u32(&full[s]));
+      tma_2d_pair(base, &ta, bar, kt * BKB, tm * 256 + rank * BM);
+      tma_2d_pair(base + A_BYTES, &tb, bar, kt * BKB, tn * BN + rank * (BN / 2));
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1 && lane == 0 && rank == 0) {
     for (int kt = 0; kt < nk; ++kt) {
       const int s = kt % STAGES;
       mbar_wait(&full[s], (kt / STAGES) & 1);
@@ -108,19 +130,19 @@ __global__ void __launch_bounds__(NT, 1)
       for (int k = 0; k < BKB / 32; ++k) {
         const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+                     "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
                      ::"r"(tmem), "l"(da + 2 * k), "l"(db + 2 * k), "r"(IDESC), "r"(acc));
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&empty[s]))
-                   : "memory");
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                   ::"r"(smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(accf))
-                 : "memory");
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                 ::"r"(smem_u32(accf)), "h"(static_cast<uint16_t>(3)) : "memory");
   } else if (warp >= 4) {
     mbar_wait(accf, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
     const int q = warp - 4;  // TMEM lane quarter
-    const int row = tm * BM + q * 32 + lane;
+    const int row = tm * 256 + rank * BM + q * 32 + lane;
     for (int c0 = 0; c0 < BN; c0 += 32) {
       uint32_t v[32];
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + c0;
@@ -142,8 +164,8 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-  __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
+  cluster_sync();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
 }
 
 typedef CUresult (*EncFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -172,9 +194,9 @@ static void run(EncFn enc, int M, int N, int K, bool check, int reps) {
   CK(cudaMalloc(&dC, sizeof(int32_t) * M * N));
   CK(cudaMemcpy(dA, hA.data(), hA.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, hB.data(), hB.size(), cudaMemcpyHostToDevice));
-  CUtensorMap ta = make_map(enc, dA, M, K, BM), tb = make_map(enc, dB, N, K, BN);
-  dim3 grid(N / BN, M / BM);
-  i8_gemm<<<grid, NT, SMEM>>>(ta, tb, M, N, K, dC);
+  CUtensorMap ta = make_map(enc, dA, M, K, BM), tb = make_map(enc, dB, N, K, BN / 2);
+  dim3 grid(2 * (N / BN), M / 256);
+  i8_gemm2<<<grid, NT, SMEM>>>(ta, tb, M, N, K, dC);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   if (check) {
@@ -195,7 +217,7 @@ static void run(EncFn enc, int M, int N, int K, bool check, int reps) {
   if (reps > 0) {
     cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0));
-    for (int r = 0; r < reps; ++r) i8_gemm<<<grid, NT, SMEM>>>(ta, tb, M, N, K, dC);
+    for (int r = 0; r < reps; ++r) i8_gemm2<<<grid, NT, SMEM>>>(ta, tb, M, N, K, dC);
     CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
     const double ops = 2.0 * M * N * double(K) * reps;
@@ -210,12 +232,12 @@ int main(int argc, char **argv) {
   void *fn = nullptr; cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
   EncFn enc = reinterpret_cast<EncFn>(fn);
-  CK(cudaFuncSetAttribute(i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CK(cudaFuncSetAttribute(i8_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   if (sustain > 0) {
     run(enc, 2048, 2048, 40960, false, sustain);
     return 0;
   }
-  run(enc, 128, 256, 128, true, 0);
+  run(enc, 256, 256, 128, true, 0);
   run(enc, 256, 512, 1024, true, 0);
   run(enc, 2048, 2048, 40960, true, 3);
   run(enc, 4096, 4096, 8192, false, 5);
