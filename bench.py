@@ -50,8 +50,7 @@ def ncu_traffic(workload: str, batch: int, kernel: str = "rform"):
     """DRAM bytes (read + write) per launch of the dominant kernel from the newest committed full ncu
     capture (profiles/rNN_ncu_kernels.json, written by tools/summarize_profiles.py), when that
     capture was taken on the same workload and energies per launch; else None. Several captured
-    kernels matching `kernel` (the INT8 GEMM runs as a diagonal-block and a CTA-pair launch per
-    chunk) are summed."""
+    kernels matching `kernel` in one capture are summed."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_kernels.json")), reverse=True):
         try:
@@ -383,14 +382,14 @@ def main():
             ach_i8 = ops_i8 / (ms_g / 1e3) / 1e12 if ms_g > 0 else None
             # DRAM bytes per GEMM launch (one chunk of 8 energies: librmx kInt8Chunk)
             traffic, traffic_src = ncu_traffic(args.config, min(batch, 8), kernel="oz_gemm")
-            roofline = {"bound": "tensor", "kernel": "oz_gemm2_kernel (CTA pairs, blocks above the diagonal) + oz_gemm_kernel (diagonal blocks): INT8 tcgen05, 16 moduli, CRT R formation",
+            roofline = {"bound": "tensor", "kernel": "oz_gemm2_kernel (INT8 tcgen05 cta_group::2, 256x256 upper-triangle blocks, 16 moduli, CRT R formation)",
                         "achieved": ach_i8, "peak": peak_i8, "unit": "TOPS",
                         "frac": (ach_i8 / peak_i8) if ach_i8 else None,
                         "traffic": traffic, "traffic_source": traffic_src,
                         "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (nominal int8/bf16 ratio, "
                                        "B200_PROFILING.md); nominal dense int8 4500 TOPS",
                         "algorithmic": "16 x nch(nch+1) x nlev int8 ops per energy x energies per launch",
-                        "traffic_per": "one chunk = the two GEMM launches over 8 energies (algorithmic bytes: 8 x 16 x nch x nlev "
+                        "traffic_per": "one oz_gemm2 launch = 8 energies (algorithmic bytes: 8 x 16 x nch x nlev "
                                        "X residues + 16 x nch x nlev W residues)"}
             r_form = {"algo": "int8-crt (rint8.cu)", "fp64_equivalent_tflops": achieved_r,
                       "vs_fp64_dmma_peak": (achieved_r / FP64_DMMA_PEAK_TFLOPS) if achieved_r else None,

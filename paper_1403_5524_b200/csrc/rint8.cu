@@ -416,8 +416,8 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
 }
 
-// CTA-pair variant (tcgen05 cta_group::2) for the blocks strictly above the diagonal: one 2-CTA
-// cluster per 256 x 256 output block (I2, J), J > I2, M = 256 per MMA instruction. CTA r stages its
+// CTA-pair variant (tcgen05 cta_group::2), the default for nch > 256: one 2-CTA cluster per 256 x 256
+// upper-triangle output block (I2, J), J >= I2, M = 256 per MMA instruction. CTA r stages its
 // own 128 rows of V (rows I2*256 + 128 r) and 128 of the 256 U rows (J*256 + 128 r) - the pair shares
 // operands, so each SM moves half the B bytes of the 1-SM kernel through shared memory (sustained INT8
 // throughput under the power cap +6 %, tools/tc_i8_gemm2.cu). Both CTAs' TMA completions count on the
@@ -754,22 +754,22 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     return cudaErrorInvalidValue;
   }
 
-  // Upper-triangle tiles - static per nch. With the CTA-pair kernel: the 256 x 256 blocks strictly
-  // above the diagonal go to oz_gemm2_kernel (list `pair`, (I2, J) in 256-blocks), the diagonal blocks
-  // to oz_gemm_kernel as two 128 x 256 tiles each (the second a half tile). Without it (a single
-  // 256-block, or RMX_I8_NOPAIR set - an A/B switch for measurements): 128 x 256 tiles throughout.
+  // Upper-triangle tiles - static per nch. CTA-pair kernel: every 256 x 256 block (I2, J), J >= I2 (the
+  // diagonal blocks compute their lower-left 128 x 128 quarter too, 6 % more MMA work at darc, which
+  // measured far cheaper than a separate 1-SM launch for them: that second pass re-read the X
+  // residues from HBM and kept the GEMMs at the power cap - DESIGN.md §5.5). 1-SM kernel (128 x 256
+  // tiles, half tiles below the diagonal): nch <= 256, or RMX_I8_NOPAIR set (an A/B switch).
   static const bool no_pair = getenv("RMX_I8_NOPAIR") != nullptr;
   const bool use_pair = !no_pair && nch > i8::BN;
   std::vector<int2> tl, pl;
-  for (int I = 0; I * i8::BM < nch; ++I)
-    for (int J = 0; J * i8::BN < nch; ++J) {
-      if (J * i8::BN + i8::BN - 1 < I * i8::BM) continue;  // entirely below the diagonal
-      if (use_pair && J > I / 2) continue;                   // inside a pair block
-      tl.push_back(make_int2(I, J));
-    }
-  if (use_pair)
+  if (use_pair) {
     for (int I2 = 0; I2 * 256 < nch; ++I2)
-      for (int J = I2 + 1; J * i8::BN < nch; ++J) pl.push_back(make_int2(I2, J));
+      for (int J = I2; J * i8::BN < nch; ++J) pl.push_back(make_int2(I2, J));
+  } else {
+    for (int I = 0; I * i8::BM < nch; ++I)
+      for (int J = 0; J * i8::BN < nch; ++J)
+        if (J * i8::BN + i8::BN - 1 >= I * i8::BM) tl.push_back(make_int2(I, J));  // not entirely below
+  }
   if (tl.size() + pl.size() > 4096) {
     err = "rform int8: nch too large for the tile list";
     return cudaErrorInvalidValue;
@@ -835,9 +835,10 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     if (c + 1 < nchunks) convert(c + 1);
     cudaStreamWaitEvent(st, ss.conv_done[b], 0);
     gemm_mark(true);
-    i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
-        tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc,
-        static_cast<int>(n));
+    if (ntiles > 0)
+      i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
+          tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc,
+          static_cast<int>(n));
     if (npair > 0)
       i8::oz_gemm2_kernel<<<static_cast<unsigned>(2 * npair * i8::L * n), i8::GEMM_NT, i8::GEMM2_SMEM, st>>>(
           tv[b], tu2, static_cast<int>(nch), static_cast<int>(nlev), npair, tiles + ntiles, ldr, res, idesc2,

@@ -42,6 +42,36 @@ def test_int8_R_matches_oracle(ctx, nch, nlev, seed):
     assert worst < 1e-12, worst
 
 
+_NOPAIR_SCRIPT = r"""
+import numpy as np, torch, oracle, rmx_synth as syn, paper_1403_5524_b200 as rmx
+ctx = rmx.Context(); ctx.set_r_algo(rmx.R_INT8)
+c = syn.brute_force_case(529, 300, 9, ne=5, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
+R, st = ctx.build_R(c.w, c.Ek, c.a, c.E); torch.cuda.synchronize(); R = R.cpu().numpy()
+assert np.all(st.cpu().numpy() == 0) and np.array_equal(R, np.swapaxes(R, 1, 2))
+w = 0.0
+for p, E in enumerate(c.E):
+    ref, _ = oracle.R(c.w, c.Ek, c.a, E)
+    w = max(w, float(np.max(np.abs(R[p] - ref)) / np.max(np.abs(ref))))
+print("WORST", w)
+"""
+
+
+def test_int8_one_sm_kernel_layout():
+    """The 1-SM GEMM layout (128 x 256 tiles, half tiles below the diagonal) that RMX_I8_NOPAIR selects
+    for nch > 256 (the default there is the CTA-pair kernel; nch = 256 above runs the 1-SM kernel by
+    default) - in a subprocess, since the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RMX_I8_NOPAIR="1")
+    out = subprocess.run([sys.executable, "-c", _NOPAIR_SCRIPT], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    worst = float(out.stdout.split("WORST")[-1])
+    assert worst < 1e-12, worst
+
+
 def test_int8_pole_status(ctx):
     import torch
     c = syn.brute_force_case(260, 300, 9, ne=4, lo=1.0, hi=5.0)
