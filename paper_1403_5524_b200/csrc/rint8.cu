@@ -693,6 +693,19 @@ int64_t rint8_ldv(int64_t nlev) { return (nlev + 15) & ~static_cast<int64_t>(15)
 int64_t rint8_ldr(int64_t nch) { return (nch + 255) & ~static_cast<int64_t>(255); }
 int rint8_max_nlev() { return 131071; }
 
+// Energies per chunk: 8, or more when one chunk's GEMM grid would be short (few 256-blocks, e.g.
+// config bp: 3 pair blocks -> 768 CTAs per 8 energies, 5.2 waves with a 0.8-wave tail), up to 64 and
+// within ~24 GB of double-buffered X residues.
+int64_t rint8_chunk(int64_t nch, int64_t nlev, int64_t ne, int nsm) {
+  const int64_t nb = (nch + 255) / 256;
+  const int64_t ctas_per_energy = 2 * (nb * (nb + 1) / 2) * 16;
+  const int64_t want = (16 * static_cast<int64_t>(nsm) + ctas_per_energy - 1) / ctas_per_energy;
+  int64_t chunk = std::max<int64_t>(8, std::min<int64_t>(64, (want + 7) / 8 * 8));
+  const int64_t per_energy = 2 * 16 * nch * rint8_ldv(nlev);
+  while (chunk > 8 && chunk * per_energy > (static_cast<int64_t>(24) << 30)) chunk -= 8;
+  return std::min(chunk, ne);
+}
+
 // Workspace (bytes) for chunks of ne energies, double-buffered (V planes, d, dmax, shifts, pole flags)
 // plus the W residues, one residue-plane buffer and the tile list
 size_t rint8_ws_bytes(int64_t nch, int64_t nlev, int64_t ne) {
@@ -813,11 +826,11 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
                                                                       dmax[b], pflag[b], stc);
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
     cudaMemsetAsync(xmax[b], 0, sizeof(float) * chunk * nch, cs);
-    i8::oz_xmax_kernel<<<dim3(static_cast<unsigned>((nch + i8::XM_ROWS - 1) / i8::XM_ROWS), i8::XM_KSPLIT), 256, 0,
-                         cs>>>(
-        w, ldw, static_cast<int>(nch),
-                                                                       static_cast<int>(nlev), static_cast<int>(n),
-                                                                       dbuf[b], xmax[b]);
+    for (int64_t q = 0; q < n; q += 8)  // the row-maxima kernel stages at most 8 energies
+      i8::oz_xmax_kernel<<<dim3(static_cast<unsigned>((nch + i8::XM_ROWS - 1) / i8::XM_ROWS), i8::XM_KSPLIT), 256,
+                           0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
+                                    static_cast<int>(std::min<int64_t>(8, n - q)), dbuf[b] + q * nlev,
+                                    xmax[b] + q * nch);
     if (x_signed)
       i8::oz_convert_kernel<true><<<g, 256, 0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
                                                          static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX, ldv,

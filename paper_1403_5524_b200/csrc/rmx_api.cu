@@ -262,7 +262,7 @@ static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double
                           int64_t nlev, double a, const double *E, int64_t ne, double *R, int32_t *status,
                           std::string &err, int *nl) {
   if (c->r_algo == RMX_R_INT8 && nlev <= rint8_max_nlev() && nch >= kInt8MinChannels) {
-    const int64_t chunk = std::min<int64_t>(ne, kInt8Chunk);
+    const int64_t chunk = rint8_chunk(nch, nlev, ne, c->nsm);
     const size_t need = rint8_ws_bytes(nch, nlev, chunk);
     if (grow(c, c->dz, need) != RMX_OK) {
       err = "INT8-CRT workspace allocation failed";

@@ -57,7 +57,7 @@ bool encode_tmap_f64(CUtensorMap *map, const double *base, int64_t rows, int64_t
 
 // rint8.cu: R formation on the INT8 tensor cores by CRT (exact integer arithmetic after a 55/53-bit
 // fixed-point rounding of X = W diag(d) and W); ws: rint8_ws_bytes(nch, nlev, chunk) bytes
-constexpr int64_t kInt8Chunk = 8;
+constexpr int64_t kInt8Chunk = 8;  // minimum energies per INT8 chunk (rint8_chunk may take more)
 // below this many channels the 128 x 256 INT8 tiles and the conversion pass do not pay off (measured:
 // config small, nch 64: DMMA 3.2e5 E/s vs INT8 1.3e5 E/s; bp, nch 500: INT8 +30 %): R_INT8 falls back
 constexpr int64_t kInt8MinChannels = 256;  // energies per INT8-CRT pass (V planes: 16 nch nlev bytes each)
@@ -65,6 +65,7 @@ int64_t rint8_ldv(int64_t nlev);
 int64_t rint8_ldr(int64_t nch);
 int rint8_max_nlev();
 size_t rint8_ws_bytes(int64_t nch, int64_t nlev, int64_t ne);
+int64_t rint8_chunk(int64_t nch, int64_t nlev, int64_t ne, int nsm);
 struct Int8Streams {  // auxiliary stream + events of the conversion / GEMM pipeline (owned by the ctx)
   cudaStream_t aux = nullptr;
   cudaEvent_t start = nullptr, conv_done[2] = {nullptr, nullptr}, gemm_done[2] = {nullptr, nullptr};
