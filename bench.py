@@ -292,6 +292,27 @@ def main():
         fk += float(np.sum(b))
         ft += float(np.sum(c))
     achieved_r = fr / (ms_r / 1e3) / 1e12 if ms_r > 0 else None
+    # ---- the per-energy dense LA kernels (matching, T epilogue): executed algorithmic flops of the
+    # routes in DESIGN.md §5.2/§5.3 (truncated back substitution; S^-1 route), the SURVEY §8(d) counts
+    # beside them, FP64 DMMA fraction, and HBM GB/s from the committed ncu capture's bytes per launch
+    fk_x, ft_x = 0.0, 0.0
+    for s in range(args.warmup, nsteps):
+        no = step_inputs[s]["no_host"].astype(np.float64)
+        fk_x += float(np.sum((2.0 / 3.0) * nch ** 3 + nch ** 2 * no + no ** 3))
+        ft_x += float(np.sum(3.0 * no ** 3))
+    la = {}
+    for kname, key, fx, fs in (("match_kernel", "match", fk_x, fk), ("tepi_kernel", "tepi", ft_x, ft)):
+        ms_k, n_k = stats.get(key, (0.0, 0))
+        if ms_k <= 0:
+            continue
+        tb, tsrc = ncu_traffic(args.config, batch, kernel=kname)
+        la[key] = {"ms": round(ms_k, 3), "launches": n_k,
+                   "tflops_executed": fx / (ms_k / 1e3) / 1e12, "tflops_survey_count": fs / (ms_k / 1e3) / 1e12,
+                   "frac_fp64_dmma_peak": fx / (ms_k / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
+                   "hbm_gbs": (tb * n_k / (ms_k / 1e3) / 1e9) if tb else None,
+                   "hbm_frac": (tb * n_k / (ms_k / 1e3) / 1e9 / float(measured_peaks().get("hbm_gbs", 6543.7)))
+                   if tb else None,
+                   "traffic_source": tsrc}
     path_tflops = (fr + fk + ft) / (ms / 1e3) / 1e12
     ms_g, n_g = stats.get("i8gemm", (0.0, 0))
 
@@ -419,6 +440,7 @@ def main():
             "roofline": roofline,
             "r_formation": r_form,
             "kernel_ms": {k: round(v[0], 3) for k, v in stats.items() if k != "launches"},
+            "la_kernels": la,
             "path_fp64_tflops": path_tflops,
             ("path_fp64_frac" if r_form["algo"].startswith("fp64") else "path_fp64_equivalent_vs_dmma_peak"):
                 path_tflops / FP64_DMMA_PEAK_TFLOPS,
