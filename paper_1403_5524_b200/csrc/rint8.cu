@@ -814,9 +814,7 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   cudaEventRecord(ss.start, st);
   cudaStreamWaitEvent(ss.aux, ss.start, 0);
   const int64_t nchunks = (ne + chunk - 1) / chunk;
-  // experiment switch: RMX_I8_SERIAL runs the conversion on the GEMM stream (no overlap)
-  static const bool serial = getenv("RMX_I8_SERIAL") != nullptr;
-  cudaStream_t cs = serial ? st : ss.aux;
+  cudaStream_t cs = ss.aux;  // conversion stream (the GEMM-stream variant measured the same: DESIGN.md §9)
   auto convert = [&](int64_t c) {
     const int b = static_cast<int>(c & 1);
     const int64_t e0 = c * chunk, n = std::min(chunk, ne - e0);
