@@ -106,6 +106,7 @@ struct GemmArgs {
   // k < i (k starts at the output tile's first row); 2 B(j, k) = 0 for k < j (k starts at the
   // output tile's first column). Whole BK slices are skipped; the rest must hold explicit zeros.
   int kband;
+  bool add_c;  // with read_c: C += A.B instead of C -= A.B (tools/gemm2_proto.cuh experiment only)
 };
 
 // C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).

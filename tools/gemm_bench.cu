@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(NT, 1) bench_kernel(double *ws, int64_t slot, 
 
 template <bool AK, bool BK_>
 __global__ void __launch_bounds__(proto::NT2, 1) bench2_kernel(double *ws, int64_t slot, int ld, int M, int N, int K,
-                                                              const CUtensorMap *maps, int reps, int64_t cofs) {
+                                                              const CUtensorMap *maps, int reps, int64_t cofs, bool readc_ = false) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t *al = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   proto::Sync2 *sy = reinterpret_cast<proto::Sync2 *>(al + proto::ST2 * proto::STAGE2);
@@ -46,8 +46,14 @@ __global__ void __launch_bounds__(proto::NT2, 1) bench2_kernel(double *ws, int64
   const int64_t msz = static_cast<int64_t>(2048) * ld;
   const MatView A{maps + (blockIdx.x * 3 + 0) * NVIEW, base, ld};
   const MatView B{maps + (blockIdx.x * 3 + 1) * NVIEW, base + msz, ld};
-  for (int r = 0; r < reps; ++r)
-    proto::gemm2_set<AK, BK_>(M, N, K, Op{A, 0, 0, AK}, Op{B, 0, 0, BK_}, base + cofs, ld, al, sy);
+  for (int r = 0; r < reps; ++r) {
+    if (cofs < 0) {  // mode 3: the full-featured variant behind a non-inlined call (C read when readc_)
+      GemmArgs ga{Op{A, 0, 0, AK}, Op{B, 0, 0, BK_}, base - cofs, ld, M, N, K, false, readc_, false, 0.0};
+      proto::gemm3_call<AK, BK_>(ga, al, sy);
+    } else {
+      proto::gemm2_set<AK, BK_>(M, N, K, Op{A, 0, 0, AK}, Op{B, 0, 0, BK_}, base + cofs, ld, al, sy);
+    }
+  }
 }
 __global__ void fill_kernel(double *p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -94,7 +100,7 @@ int main(int argc, char **argv) {
   cudaMemcpy(dm, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(BenchSmem));
   const int mode = argc > 7 ? atoi(argv[7]) : 0;
-  if (mode == 2) {
+  if (mode == 2 || mode == 3) {
     // C_ref = A.B by la::gemm_set into rows 0.. of the C matrix, C_new by the prototype into rows
     // 1024.. of it (requires M <= 1024); same random A, B
     fill_kernel<<<1024, 256>>>(ws, slot * nsm);
@@ -102,19 +108,19 @@ int main(int argc, char **argv) {
     auto launch2 = [&](int reps, int64_t cofs) {
       if (akc && bkc) {
         cudaFuncSetAttribute(bench2_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, proto::SMEM2);
-        bench2_kernel<true, true><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs);
+        bench2_kernel<true, true><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs, readc);
       } else if (akc) {
         cudaFuncSetAttribute(bench2_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, proto::SMEM2);
-        bench2_kernel<true, false><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs);
+        bench2_kernel<true, false><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs, readc);
       } else if (bkc) {
         cudaFuncSetAttribute(bench2_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, proto::SMEM2);
-        bench2_kernel<false, true><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs);
+        bench2_kernel<false, true><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs, readc);
       } else {
         cudaFuncSetAttribute(bench2_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, proto::SMEM2);
-        bench2_kernel<false, false><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs);
+        bench2_kernel<false, false><<<nsm, proto::NT2, proto::SMEM2>>>(ws, slot, ld, M, N, K, dm, reps, cofs, readc);
       }
     };
-    const int64_t c_ref = 2 * msz, c_new = 2 * msz + 1024LL * ld;
+    const int64_t c_ref = 2 * msz, c_new = (mode == 3 ? -1 : 1) * (2 * msz + 1024LL * ld);
     bench_kernel<<<nsm, NT, sizeof(BenchSmem)>>>(ws, slot, ld, M, N, K, dm, akc, bkc, false, 1);
     launch2(1, c_new);
     cudaDeviceSynchronize();
@@ -122,7 +128,7 @@ int main(int argc, char **argv) {
     double maxd = 0.0, maxv = 0.0;
     for (int s = 0; s < nsm; s += 37) {
       cudaMemcpy(h1.data(), ws + s * slot + c_ref, sizeof(double) * M * ld, cudaMemcpyDeviceToHost);
-      cudaMemcpy(h2.data(), ws + s * slot + c_new, sizeof(double) * M * ld, cudaMemcpyDeviceToHost);
+      cudaMemcpy(h2.data(), ws + s * slot + (c_new < 0 ? -c_new : c_new), sizeof(double) * M * ld, cudaMemcpyDeviceToHost);
       for (int i = 0; i < M; ++i)
         for (int j = 0; j < N; ++j) {
           maxd = fmax(maxd, fabs(h1[(size_t)i * ld + j] - h2[(size_t)i * ld + j]));
@@ -135,7 +141,7 @@ int main(int argc, char **argv) {
     cudaEventCreate(&f1);
     float ms_old, ms_new;
     cudaEventRecord(f0);
-    bench_kernel<<<nsm, NT, sizeof(BenchSmem)>>>(ws, slot, ld, M, N, K, dm, akc, bkc, false, reps2);
+    bench_kernel<<<nsm, NT, sizeof(BenchSmem)>>>(ws, slot, ld, M, N, K, dm, akc, bkc, readc, reps2);
     cudaEventRecord(f1);
     cudaEventSynchronize(f1);
     cudaEventElapsedTime(&ms_old, f0, f1);
