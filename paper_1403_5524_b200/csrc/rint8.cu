@@ -1,7 +1,7 @@
 // rint8.cu - R formation on the INT8 tensor cores (tcgen05.mma kind::i8) with exact FP64-level
 // accuracy, by the Chinese-remainder (Ozaki-II-style) emulation of the fp64 contraction
 //     R_ij(E) = (1/2a) sum_k w_ik w_jk / (E_k - E)          (Eq. 1-2; BASELINE.json:5)
-// (readings Z1-Z3). Same C-ABI semantics as rform.cu; selected per context.
+// (reading Z1). Same C-ABI semantics as rform.cu; selected per context.
 //
 //   1. d_k(E) = 1/(E_k - E) and dmax(E) = max_k |d_k| (pole guard as everywhere: |E - E_k| < 1e-10).
 //   2. Fixed-point operands (exact integers):  X'_ik = rint(w_ik d_k 2^{s_i}),  |X'| <= 2^54, with
@@ -10,7 +10,9 @@
 //      M = prod of the 16 pairwise-coprime moduli below (2^125.19).
 //   3. For each modulus m_l: V_l = X' mod m_l (uint8 in [0, m); balanced int8 when nlev > 65000),
 //      U_l = W' mod m_l as balanced int8 (|.| <= 128); the INT8 tensor-core GEMM C_l = V_l U_l^T is
-//      exact in int32 (|C| <= 255 * 128 nlev < 2^31), its residue C_l mod m_l = P mod m_l.
+//      exact in int32 (|C| <= 255 * 128 nlev < 2^31), its residue C_l mod m_l = P mod m_l. The GEMM
+//      runs as CTA pairs (tcgen05.mma.cta_group::2, one 2-SM cluster per 256 x 256 upper-triangle
+//      block: oz_gemm2_kernel); the 1-SM 128 x 256-tile kernel oz_gemm_kernel serves nch <= 256.
 //   4. CRT (direct formula, exact 128-bit wrapping arithmetic) recovers P_ij in (-M/2, M/2); then
 //      R_ij = P_ij 2^{-s_i - t_j} / (2a), upper triangle mirrored (bitwise symmetric R).
 // The only approximation is the rounding of X and W to 55 / 53 significant bits relative to the row
