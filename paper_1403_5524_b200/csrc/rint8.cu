@@ -447,9 +447,10 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
-    oz_gemm2_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu2, int nch,
-                    int nlev, int ntiles, const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res,
-                    uint32_t idesc, int nen) {
+    oz_gemm2_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu2,
+                    const __grid_constant__ CUtensorMap tun, int nch, int nlev, int ntiles,
+                    const int2 *__restrict__ tiles, int64_t ldr, uint8_t *__restrict__ res, uint32_t idesc, int nen,
+                    int jlast, int nlast) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + P_STAGES * P_STAGE_BYTES);
@@ -466,7 +467,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
   const int nk = (nlev + BKB - 1) / BKB;
   const int row0 = tij.x * 256 + static_cast<int>(rank) * BM;
   const int vrow = static_cast<int>((e * L + l) * nch) + row0;
-  const int urow = l * nch + tij.y * BN + static_cast<int>(rank) * (BN / 2);
+  // the ragged last column block (nch - jlast*256 columns) runs as N = nlast (a multiple of 16):
+  // each CTA of the pair then holds nlast/2 of its W rows (tensor map tun, boxes of nlast/2 rows)
+  const bool edge = tij.y == jlast && nlast < BN;
+  const int nb2 = edge ? nlast / 2 : BN / 2;
+  const CUtensorMap *tb = edge ? &tun : &tu2;
+  const uint32_t idesc_k = edge ? ((idesc & ~(0x3Fu << 17)) | (static_cast<uint32_t>(nlast >> 3) << 17)) : idesc;
+  const uint32_t stage_tx = 2u * static_cast<uint32_t>(A_BYTES + nb2 * BKB);
+  const int urow = l * nch + tij.y * BN + static_cast<int>(rank) * nb2;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P_STAGES; ++s) {
@@ -488,11 +496,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tv);
-    tma_prefetch_desc(&tu2);
+    tma_prefetch_desc(tb);
     for (int kt = 0; kt < nk; ++kt) {
       const int s = kt % P_STAGES;
       if (kt >= P_STAGES) mbar_wait(&empty[s], ((kt / P_STAGES) - 1) & 1);
-      if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+      if (rank == 0) mbar_arrive_expect_tx(&full[s], stage_tx);
       const uint32_t base = smem_u32(smem + s * P_STAGE_BYTES);
       const uint32_t bar = mapa_rank0(smem_u32(&full[s]));
       asm volatile(
@@ -502,7 +510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
           : "memory");
       asm volatile(
           "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(base + A_BYTES), "l"(reinterpret_cast<uint64_t>(&tu2)), "r"(bar),
+          " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(base + A_BYTES), "l"(reinterpret_cast<uint64_t>(tb)), "r"(bar),
           "r"(kt * BKB), "r"(urow)
           : "memory");
     }
@@ -518,7 +526,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
         const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
+                     "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc_k), "r"(acc));
       }
       asm volatile(
           "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
@@ -806,6 +814,13 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   if (!encode_i8(&tu, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, i8::BN, err)) return cudaErrorInvalidValue;
   CUtensorMap tu2;  // U rows in boxes of 128 (one half of a pair block's columns per CTA)
   if (!encode_i8(&tu2, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, i8::BN / 2, err)) return cudaErrorInvalidValue;
+  // ragged last column block: N = nlast = round16(nch - jlast*256), nlast/2 W rows per CTA
+  const int jlast = static_cast<int>((nch - 1) / i8::BN);
+  const int nlast = static_cast<int>(std::max<int64_t>(16, ((nch - static_cast<int64_t>(jlast) * i8::BN) + 15) / 16 * 16));
+  CUtensorMap tun = tu2;
+  if (nlast < i8::BN &&
+      !encode_i8(&tun, U, static_cast<int64_t>(i8::L) * nch, nlev, ldv, nlast / 2, err))
+    return cudaErrorInvalidValue;
   for (int b = 0; b < 2; ++b)
     if (!encode_i8(&tv[b], V[b], chunk * i8::L * nch, nlev, ldv, i8::BM, err)) return cudaErrorInvalidValue;
   const double inv2a = 1.0 / (2.0 * a);
@@ -854,8 +869,8 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
           static_cast<int>(n));
     if (npair > 0)
       i8::oz_gemm2_kernel<<<static_cast<unsigned>(2 * npair * i8::L * n), i8::GEMM_NT, i8::GEMM2_SMEM, st>>>(
-          tv[b], tu2, static_cast<int>(nch), static_cast<int>(nlev), npair, tiles + ntiles, ldr, res, idesc2,
-          static_cast<int>(n));
+          tv[b], tu2, tun, static_cast<int>(nch), static_cast<int>(nlev), npair, tiles + ntiles, ldr, res, idesc2,
+          static_cast<int>(n), jlast, nlast);
     gemm_mark(false);
     dim3 gc(static_cast<unsigned>((nch + 1 + 255) / 256), static_cast<unsigned>((nch + 1) / 2),
             static_cast<unsigned>(n));
