@@ -561,33 +561,10 @@ struct CrtConst {
 };
 __constant__ CrtConst c_crt;
 
-__global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t *__restrict__ res, int64_t ldr, int nch,
-                                                     const int32_t *__restrict__ sx, const int32_t *__restrict__ tw,
-                                                     double inv2a, const int32_t *__restrict__ pflag,
-                                                     double *__restrict__ R) {
-  // rows i and nch-1-i share a block row (upper triangle: nch+1 entries per pair of rows)
-  const int64_t e = blockIdx.z;
-  const int pr = blockIdx.y;  // row pair
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int len0 = nch - pr;  // entries j >= i of row pr
-  int i, j;
-  if (t < len0) {
-    i = pr;
-    j = pr + t;
-  } else {
-    i = nch - 1 - pr;
-    j = i + (t - len0);
-    if (i <= pr || j >= nch) return;
-  }
-  double *Re = R + e * static_cast<int64_t>(nch) * nch;
-  if (pflag[e]) {
-    const double nan = __longlong_as_double(0x7ff8000000000000LL);
-    Re[static_cast<int64_t>(i) * nch + j] = nan;
-    Re[static_cast<int64_t>(j) * nch + i] = nan;
-    return;
-  }
-  const int64_t plane = static_cast<int64_t>(nch) * ldr;
-  const uint8_t *rp = res + e * L * plane + static_cast<int64_t>(i) * ldr + j;
+// CRT on 32 x 32 tiles of the upper triangle (one CTA per tile and energy, 256 threads x 4 rows):
+// residue loads and the R[i][j] stores run along j, and the mirrored R[j][i] half is written from a
+// shared-memory transpose along i (coalesced in both directions).
+__device__ __forceinline__ double crt_value(const uint8_t *rp, int64_t plane, int s_sum, double inv2a) {
   uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
   double sf = 0.0;
 #pragma unroll
@@ -599,13 +576,11 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t *__restrict__
     a3 += static_cast<uint64_t>(r) * c_crt.C[l][3];
     sf = fma(static_cast<double>(r), c_crt.f[l], sf);
   }
-  // S mod 2^128 from the limb sums (each < 2^44)
   a1 += a0 >> 32;
   a2 += a1 >> 32;
   a3 += a2 >> 32;
   uint64_t lo = (a0 & 0xFFFFFFFFull) | (a1 << 32);
   uint64_t hi = (a2 & 0xFFFFFFFFull) | (a3 << 32);
-  // - q M
   const uint64_t q = static_cast<uint64_t>(rint(sf));
   const uint64_t m01 = (static_cast<uint64_t>(c_crt.M[1]) << 32) | c_crt.M[0];
   const uint64_t m23 = (static_cast<uint64_t>(c_crt.M[3]) << 32) | c_crt.M[2];
@@ -614,15 +589,55 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t *__restrict__
   hi = hi - qhi - (lo < qlo ? 1ull : 0ull);
   lo = nlo;
   const bool neg = static_cast<int64_t>(hi) < 0;
-  if (neg) {  // negate the 128-bit two's complement value
+  if (neg) {
     lo = ~lo + 1;
     hi = ~hi + (lo == 0 ? 1ull : 0ull);
   }
   double p = static_cast<double>(hi) * 18446744073709551616.0 + static_cast<double>(lo);
   if (neg) p = -p;
-  const double r = ldexp(p, -(sx[e * nch + i] + tw[j])) * inv2a;
-  Re[static_cast<int64_t>(i) * nch + j] = r;
-  Re[static_cast<int64_t>(j) * nch + i] = r;
+  return ldexp(p, -s_sum) * inv2a;
+}
+
+__global__ void __launch_bounds__(256) oz_crt_tile_kernel(const uint8_t *__restrict__ res, int64_t ldr, int nch,
+                                                          const int32_t *__restrict__ sx,
+                                                          const int32_t *__restrict__ tw, double inv2a,
+                                                          const int32_t *__restrict__ pflag, double *__restrict__ R) {
+  __shared__ double tile[32][33];
+  const int64_t e = blockIdx.y;
+  // blockIdx.x enumerates the upper-triangle tiles (ti <= tj) row by row
+  const int nt = (nch + 31) / 32;
+  int ti = 0, rem = blockIdx.x;
+  while (rem >= nt - ti) {
+    rem -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + rem;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double *Re = R + e * static_cast<int64_t>(nch) * nch;
+  const int64_t plane = static_cast<int64_t>(nch) * ldr;
+  const bool pole = pflag[e] != 0;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  const int j = tj * 32 + tx;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int li = ty + 8 * q, i = ti * 32 + li;
+    double v = 0.0;
+    if (i < nch && j < nch && j >= i) {
+      v = pole ? nan
+               : crt_value(res + e * L * plane + static_cast<int64_t>(i) * ldr + j, plane,
+                           sx[e * nch + i] + tw[j], inv2a);
+      Re[static_cast<int64_t>(i) * nch + j] = v;
+    }
+    tile[li][tx] = v;
+  }
+  __syncthreads();
+  // mirror: R[j][i] = R[i][j] for i < j, written along i
+  const int i2 = ti * 32 + tx;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int lj = ty + 8 * q, j2 = tj * 32 + lj;
+    if (i2 < nch && j2 < nch && i2 < j2) Re[static_cast<int64_t>(j2) * nch + i2] = tile[tx][lj];
+  }
 }
 
 }  // namespace i8
@@ -872,10 +887,10 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
           tv[b], tu2, tun, static_cast<int>(nch), static_cast<int>(nlev), npair, tiles + ntiles, ldr, res, idesc2,
           static_cast<int>(n), jlast, nlast);
     gemm_mark(false);
-    dim3 gc(static_cast<unsigned>((nch + 1 + 255) / 256), static_cast<unsigned>((nch + 1) / 2),
-            static_cast<unsigned>(n));
-    i8::oz_crt_kernel<<<gc, 256, 0, st>>>(res, ldr, static_cast<int>(nch), sx[b], tw, inv2a, pflag[b],
-                                          R + e0 * nch * nch);
+    const int64_t ntc = (nch + 31) / 32;
+    dim3 gc(static_cast<unsigned>(ntc * (ntc + 1) / 2), static_cast<unsigned>(n));
+    i8::oz_crt_tile_kernel<<<gc, 256, 0, st>>>(res, ldr, static_cast<int>(nch), sx[b], tw, inv2a, pflag[b],
+                                               R + e0 * nch * nch);
     cudaEventRecord(ss.gemm_done[b], st);  // after the CRT: it reads sx[b] and pflag[b]
     ce = cudaGetLastError();
     if (ce != cudaSuccess) return ce;
