@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
 // throughput under the power cap +6 %, tools/tc_i8_gemm2.cu). Both CTAs' TMA completions count on the
 // leader's full barrier; the leader's single MMA thread commits each stage to both CTAs' empty
 // barriers and the finished accumulator to both accf barriers; each CTA drains its own TMEM rows.
-constexpr int P_STAGES = 6;
+constexpr int P_STAGES = 7;
 constexpr int P_B_BYTES = (BN / 2) * BKB, P_STAGE_BYTES = A_BYTES + P_B_BYTES;
 constexpr int GEMM2_SMEM = 1024 + P_STAGES * P_STAGE_BYTES + 256;
 __host__ __device__ constexpr uint32_t idesc_i8_pair(bool a_signed) {
