@@ -6,9 +6,6 @@
 // (rotating refill, STAGES - 1 slices ahead). C = A.B only, K % 32 == 0, full tiles (bench shapes).
 // Measured against la::gemm_set by tools/gemm_bench.cu (mode 2).
 #pragma once
-#ifndef GV
-#define GV 0
-#endif
 #include "../paper_1403_5524_b200/csrc/cta_la.cuh"
 
 namespace rmx {
