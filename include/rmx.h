@@ -303,11 +303,11 @@ rmx_rc rmx_sync(rmx_ctx *ctx, const int32_t *status, int64_t ne, int64_t *n_bad)
  * rmx_set_r_algo - choose how rmx_build_R / rmx_sweep* form R on this context:
  *   RMX_R_DMMA (default): the FP64 tensor-core (DMMA) contraction of rform.cu;
  *   RMX_R_INT8: the same R by exact integer arithmetic on the INT8 tensor cores (tcgen05 kind::i8):
- *     X = W diag(d) and W rounded to 55 / 53-bit fixed point per row, 16 modular INT8 GEMMs, CRT
- *     reconstruction (rint8.cu); R error at the level of an fp64 contraction
- *     (normwise ~1e-14). Applies for nch >= 256 and nlev <= 131071 (int32 accumulator bound);
- *     otherwise the DMMA contraction is used.
- *     Workspace ~ 8 x 16 x nch x nlev bytes.
+ *     X = W diag(d) and W rounded to 55 / 53-bit fixed point per row, 16 modular INT8 GEMMs (CTA
+ *     pairs, tcgen05.mma.cta_group::2, for nch > 256), CRT reconstruction (rint8.cu);
+ *     R error at the level of an fp64 contraction (normwise ~1e-14). Applies for nch >= 256 and
+ *     nlev <= 131071 (int32 accumulator bound); otherwise the DMMA contraction is used.
+ *     Workspace ~ 2 x chunk x 16 x nch x nlev bytes (chunk = 8 energies, more for small nch).
  */
 enum { RMX_R_DMMA = 0, RMX_R_INT8 = 1 };
 rmx_rc rmx_set_r_algo(rmx_ctx *ctx, int algo);
