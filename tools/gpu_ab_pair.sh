@@ -1,12 +1,11 @@
 #!/usr/bin/env bash
-# INT8 GEMM layouts: pair blocks above the diagonal + 1-SM diagonal kernel (default), pair blocks
-# everywhere (RMX_I8_PAIRDIAG), 1-SM only (RMX_I8_NOPAIR); parity of the INT8 path in each.
+# INT8 GEMM layouts: CTA-pair kernel over all 256-blocks (default) vs the 1-SM 128x256-tile kernel
+# (RMX_I8_NOPAIR); INT8-path parity in each, then alternating bench lines.
 set -u
 mkdir -p gpurun_out
-for v in default pairdiag nopair default pairdiag; do
-  unset RMX_I8_NOPAIR RMX_I8_PAIRDIAG
+for v in default nopair default nopair; do
+  unset RMX_I8_NOPAIR
   [ $v = nopair ] && export RMX_I8_NOPAIR=1
-  [ $v = pairdiag ] && export RMX_I8_PAIRDIAG=1
   if [ ! -f gpurun_out/ab_pytest_$v.log ]; then
     timeout 900 python -m pytest tests/test_rint8.py -x -q > gpurun_out/ab_pytest_$v.log 2>&1; echo "$v pytest rc=$?"
   fi
