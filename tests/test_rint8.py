@@ -26,7 +26,7 @@ def ctx():
 
 
 @pytest.mark.parametrize("nch,nlev,seed", [(300, 1000, 1), (403, 517, 2), (257, 77, 3), (256, 5, 4),
-                                           (529, 257, 6), (300, 2100, 7)])
+                                           (529, 257, 6), (300, 2100, 7), (512, 300, 8), (784, 129, 9)])
 def test_int8_R_matches_oracle(ctx, nch, nlev, seed):
     import torch
     c = syn.brute_force_case(nch, nlev, seed, ne=11, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
