@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# Persistent (dynamic block counter, RMX_I8_PERSIST) vs non-persistent pair GEMM: INT8 parity, DRAM
+# Persistent (dynamic block counter, RMX_I8_PERSIST - an experiment since removed from rint8.cu)
 # bytes / L2 hit per launch (ncu) and bench lines.
 set -u
 mkdir -p gpurun_out
