@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # Persistent (dynamic block counter, RMX_I8_PERSIST - an experiment since removed from rint8.cu)
-# bytes / L2 hit per launch (ncu) and bench lines.
+# vs the non-persistent pair GEMM: INT8 parity, DRAM bytes / L2 hit per launch (ncu) and bench lines.
 set -u
 mkdir -p gpurun_out
 export RMX_I8_PERSIST=1
