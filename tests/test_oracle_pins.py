@@ -81,6 +81,37 @@ def test_R_brute_force_direct_solve(seed, nch, nlev):
         assert nrel(R, direct) < 1e-9, (E, nrel(R, direct))
 
 
+def test_R_entries_pinned():
+    """oracle_R_entries (the reference of the full-size sampled R checks) against what fixes R
+    independently of the oracle: the hand-evaluated 2 x 3 case (exact, both index orders), the
+    brute force (1/2a) P^T (H - E)^{-1} P on sampled (i, j) pairs including diagonal, upper and
+    lower entries (BASELINE.json:5; Eq. 1 in the north_star convention), and
+    the pole guard. A scaled, transposed or mis-indexed sum fails one of these."""
+    w = np.array([[1.0, 2.0, 0.0], [0.0, 3.0, -1.0]])
+    Ek = np.array([0.0, 1.0, 4.0])
+    E, a = 2.0, 0.5
+    d = 1.0 / (Ek - E)
+    expect = np.array([[1 * d[0] + 4 * d[1], 6 * d[1]],
+                       [6 * d[1], 9 * d[1] + 1 * d[2]]]) / (2 * a)
+    ii, jj = np.array([0, 0, 1, 1]), np.array([0, 1, 0, 1])
+    vals, st = oracle.R_entries(w, Ek, a, E, ii, jj)
+    assert st == 0
+    np.testing.assert_allclose(vals, expect[ii, jj], rtol=1e-15, atol=1e-16)
+    rng = np.random.default_rng(11)
+    for seed, nch, nlev in [(4, 9, 60), (5, 17, 220)]:
+        c = syn.brute_force_case(nch, nlev, seed, ne=5)
+        ii = np.concatenate([np.arange(nch), rng.integers(0, nch, 40)])
+        jj = np.concatenate([np.arange(nch), rng.integers(0, nch, 40)])
+        for E in c.E:
+            direct = c.P.T @ np.linalg.solve(c.H - E * np.eye(nlev), c.P) / (2 * c.a)
+            vals, st = oracle.R_entries(c.w, c.Ek, c.a, E, ii, jj)
+            assert st == 0
+            err = np.max(np.abs(vals - direct[ii, jj])) / np.max(np.abs(direct))
+            assert err < 1e-9, (seed, E, err)
+    vals, st = oracle.R_entries(w, Ek, a, 1.0 + 1e-12, ii[:2], jj[:2])
+    assert st == 1 and np.all(np.isnan(vals))
+
+
 def test_R_small_config_is_its_own_brute_force():
     """Config 'small' (BASELINE.json:8) is generated as w = P^T V, so R(E) = (1/2a) P^T(H-E)^{-1}P
     holds for the config itself. Checked at 2 energies."""
