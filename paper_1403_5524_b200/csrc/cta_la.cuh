@@ -85,6 +85,10 @@ __device__ __forceinline__ int kc_first(int kband, int tm, int tn) {
   return kband == 1 ? (tm * BM) / BK : (kband == 2 ? (tn * BN) / BK : 0);
 }
 __device__ __forceinline__ int frag_perm(int g) { return (g >> 1) + 4 * (g & 1); }
+// x with its sign bit xor-ed with the top bit of `sgn` (0 or 0x80000000)
+__device__ __forceinline__ double flip_sign(double x, uint32_t sgn) {
+  return __hiloint2double(__double2hiint(x) ^ static_cast<int>(sgn), __double2loint(x));
+}
 
 // Producer-warp helper: bulk-copy `nrows` rows of `rbytes` bytes (16-byte multiple) from
 // G + r*ld to smem rows of pitch `ld_s` doubles; completion on bar.
@@ -107,6 +111,13 @@ struct GemmArgs {
   // output tile's first column). Whole BK slices are skipped; the rest must hold explicit zeros.
   int kband;
   bool add_c;  // with read_c: C += A.B instead of C -= A.B (tools/gemm2_proto.cuh experiment only)
+  // optional second product, summed into the first along k: A.B + (neg2 ? -1 : +1) A2.B2 (same
+  // M, N, K, kband and operand layouts as (a, b)); a complex product is two such real GEMMs
+  // (Re = Ar.Br - Ai.Bi, Im = Ar.Bi + Ai.Br), the k range doubling instead of C being re-read
+  Op a2{}, b2{};
+  int nseg = 1;
+  bool neg2 = false;
+  double alpha = 1.0;  // set mode (read_c false): C = alpha (A.B) + diag_add I
 };
 
 // C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).
@@ -148,12 +159,13 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
     // generic-proxy global writes of earlier phases (made CTA-visible by the barrier above) must be
     // ordered before the async-proxy (TMA / bulk) reads issued below
     asm volatile("fence.proxy.async;\n" ::: "memory");
-    const CUtensorMap *tmA = ga.a.v.tm + (A_KC ? 0 : 2);
-    const CUtensorMap *tmB = ga.b.v.tm + (B_KC ? 1 : 2);
-    if (lane == 0) {
-      tma_prefetch_desc(tmA);
-      tma_prefetch_desc(tmB);
-    }
+    const CUtensorMap *tmAs[2] = {ga.a.v.tm + (A_KC ? 0 : 2), ga.a2.v.tm + (A_KC ? 0 : 2)};
+    const CUtensorMap *tmBs[2] = {ga.b.v.tm + (B_KC ? 1 : 2), ga.b2.v.tm + (B_KC ? 1 : 2)};
+    if (lane == 0)
+      for (int sg = 0; sg < ga.nseg; ++sg) {
+        tma_prefetch_desc(tmAs[sg]);
+        tma_prefetch_desc(tmBs[sg]);
+      }
     int it = 0, tm = 0, tn = 0, rowcnt = tiles_in_row(0, tiles_n, lower);
     for (int tile = 0; tile < ntiles; ++tile) {
       if (tn == rowcnt) {
@@ -169,6 +181,9 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
         bulk_rows(Cs, CS_LD, ga.C + static_cast<int64_t>(tm * BM) * ga.ldc + tn * BN, ga.ldc, rows,
                   rb, &gs->cfull);
       }
+      for (int sg = 0; sg < ga.nseg; ++sg) {
+      const Op &oa = sg ? ga.a2 : ga.a, &ob = sg ? ga.b2 : ga.b;
+      const CUtensorMap *tmA = tmAs[sg], *tmB = tmBs[sg];
       for (int kc = kc_first(ga.kband, tm, tn); kc < nkc; ++kc, ++it) {
         const int st = it % STAGES, use = it / STAGES;
         if (it >= STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
@@ -180,23 +195,24 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
           if (A_KC) {
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-              tma_load_2d(sa + q * (BM * 128), tmA, bar, ga.a.c0 + k0 + 16 * q, ga.a.r0 + tm * BM);
+              tma_load_2d(sa + q * (BM * 128), tmA, bar, oa.c0 + k0 + 16 * q, oa.r0 + tm * BM);
           } else {
 #pragma unroll
             for (int q = 0; q < BM / 16; ++q)
-              tma_load_2d(sa + q * (BK * 128), tmA, bar, ga.a.c0 + tm * BM + 16 * q, ga.a.r0 + k0);
+              tma_load_2d(sa + q * (BK * 128), tmA, bar, oa.c0 + tm * BM + 16 * q, oa.r0 + k0);
           }
           if (B_KC) {
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-              tma_load_2d(sb + q * (BN * 128), tmB, bar, ga.b.c0 + k0 + 16 * q, ga.b.r0 + tn * BN);
+              tma_load_2d(sb + q * (BN * 128), tmB, bar, ob.c0 + k0 + 16 * q, ob.r0 + tn * BN);
           } else {
 #pragma unroll
             for (int q = 0; q < BN / 16; ++q)
-              tma_load_2d(sb + q * (BK * 128), tmB, bar, ga.b.c0 + tn * BN + 16 * q, ga.b.r0 + k0);
+              tma_load_2d(sb + q * (BK * 128), tmB, bar, ob.c0 + tn * BN + 16 * q, ob.r0 + k0);
           }
         }
         __syncwarp();
+      }
       }
       ++tn;
     }
@@ -270,6 +286,10 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
+      for (int sg = 0; sg < ga.nseg; ++sg) {
+      // sign of the second product: flip the sign bit of its A fragments (integer op, off the
+      // FP64 pipe)
+      const uint32_t sgn = (sg == 1 && ga.neg2) ? 0x80000000u : 0u;
       for (int kc = kc_first(ga.kband, tm, tn); kc < nkc; ++kc, ++it) {
         const int st = it % STAGES, use = it / STAGES;
         mbar_wait(&gs->full[st], use & 1);
@@ -295,6 +315,10 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
               b[ni][1] = lds64(sb + k8 * 1024 + boff[ni][1]);
             }
           }
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) a[mi][h] = flip_sign(a[mi][h], sgn);
           if (partial) {  // zero both operands beyond K (stale smem may hold anything)
             const int k = k8 * 8 + 2 * t;
             const bool v0 = k < krem, v1 = k + 1 < krem;
@@ -327,6 +351,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
         __syncwarp();
         if (lane == 0) mbar_arrive(&gs->empty[st]);
       }
+      }
       // epilogue: this warp's 32 x 32 part of the tile straight to global memory
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) {
@@ -344,7 +369,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
             else if (ga.trans_c)
               ga.C[static_cast<int64_t>(c) * ga.ldc + r] = acc[mi][ni][h];
             else
-              crow[c] = acc[mi][ni][h] + (r == c ? ga.diag_add : 0.0);
+              crow[c] = ga.alpha * acc[mi][ni][h] + (r == c ? ga.diag_add : 0.0);
           }
       }
       ++tn;

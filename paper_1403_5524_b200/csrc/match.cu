@@ -227,13 +227,8 @@ cudaError_t launch_match(const double *R, const double *F, const double *G, cons
                          const double *Gp, double a, int64_t nch, int64_t ne, const int32_t *n_open,
                          double *K, double *ws, int64_t ws_slot, const CUtensorMap *views, int64_t ws_slots,
                          int32_t *status, cudaStream_t st, int open_rows_only) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t ce = cudaFuncSetAttribute(match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sizeof(MatchSmem)));
-    if (ce != cudaSuccess) return ce;
-    attr = true;
-  }
+  cudaError_t ce = ensure_smem_attr(reinterpret_cast<const void *>(match_kernel), sizeof(MatchSmem));
+  if (ce != cudaSuccess) return ce;
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
   match_kernel<<<grid, NT, sizeof(MatchSmem), st>>>(R, nch, F, G, Fp, Gp, a, static_cast<int>(nch),
                                                     ne, n_open, K, nch, ws, ws_slot, views, status,

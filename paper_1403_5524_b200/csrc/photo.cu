@@ -120,12 +120,8 @@ cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, cons
                             int64_t nch, int64_t nlev, const double *E, int64_t ne, double *g,
                             int32_t *status, double *part, int64_t part_cap, cudaStream_t st) {
   constexpr int smem = sizeof(double) * (DG_BK * DG_LDW + DG_BK * DG_BE);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t ce = cudaFuncSetAttribute(dipole_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (ce != cudaSuccess) return ce;
-    attr = true;
-  }
+  cudaError_t ce = ensure_smem_attr(reinterpret_cast<const void *>(dipole_g_kernel), smem);
+  if (ce != cudaSuccess) return ce;
   const int64_t max_e = static_cast<int64_t>(65535) * DG_BE;  // grid.y limit
   for (int64_t e0 = 0; e0 < ne; e0 += max_e) {
     const int64_t n = ne - e0 < max_e ? ne - e0 : max_e;

@@ -478,13 +478,9 @@ static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *
     err = "cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) + ")";
     return cudaErrorInvalidValue;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t ce = cudaFuncSetAttribute(rform_dmma_kernel<C>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          C::SMEM_BYTES);
+  {
+    cudaError_t ce = ensure_smem_attr(reinterpret_cast<const void *>(rform_dmma_kernel<C>), C::SMEM_BYTES);
     if (ce != cudaSuccess) return ce;
-    attr_set = true;
   }
   const int ntiles = (nch + C::BM - 1) / C::BM;
   const int npairs = ntiles * (ntiles + 1) / 2;

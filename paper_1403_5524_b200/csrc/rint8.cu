@@ -644,10 +644,8 @@ __global__ void __launch_bounds__(256) oz_crt_tile_kernel(const uint8_t *__restr
 
 // ---------------------------------------------------------------------------------------------
 // host side
-static bool g_i8_consts = false;
-
-static cudaError_t init_i8_consts() {
-  if (g_i8_consts) return cudaSuccess;
+// __constant__ memory is per device: the tables are uploaded once per device (once_per_device)
+static cudaError_t upload_i8_consts() {
   i8::ModConst mc[i8::L];
   i8::CrtConst cc{};
   unsigned __int128 M = 1;
@@ -680,8 +678,12 @@ static cudaError_t init_i8_consts() {
   for (int k = 0; k < 4; ++k) cc.M[k] = static_cast<uint32_t>(M >> (32 * k));
   cudaError_t e = cudaMemcpyToSymbol(i8::c_mod, mc, sizeof(mc));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(i8::c_crt, &cc, sizeof(cc));
-  if (e == cudaSuccess) g_i8_consts = true;
   return e;
+}
+
+static cudaError_t init_i8_consts() {
+  static const int key = 0;
+  return once_per_device(&key, upload_i8_consts);
 }
 
 static bool encode_i8(CUtensorMap *map, const void *base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
@@ -755,14 +757,10 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
                               std::string &err, const std::function<void(bool)> &gemm_mark) {
   cudaError_t ce = init_i8_consts();
   if (ce != cudaSuccess) return ce;
-  static bool attr = false;
-  if (!attr) {
-    ce = cudaFuncSetAttribute(i8::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::GEMM_SMEM);
-    if (ce != cudaSuccess) return ce;
-    ce = cudaFuncSetAttribute(i8::oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, i8::GEMM2_SMEM);
-    if (ce != cudaSuccess) return ce;
-    attr = true;
-  }
+  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm_kernel), i8::GEMM_SMEM);
+  if (ce != cudaSuccess) return ce;
+  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel), i8::GEMM2_SMEM);
+  if (ce != cudaSuccess) return ce;
   const int64_t ldv = rint8_ldv(nlev), ldr = rint8_ldr(nch);
   uint8_t *wsp = static_cast<uint8_t *>(ws);
   auto carve = [&](size_t bytes) {

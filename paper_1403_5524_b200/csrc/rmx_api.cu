@@ -4,7 +4,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cublas_v2.h>
@@ -13,6 +16,19 @@
 #include "rmx_internal.h"
 
 using namespace rmx;
+
+cudaError_t rmx::once_per_device(const void *key, const std::function<cudaError_t()> &init) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({key, dev})) return cudaSuccess;
+  e = init();
+  if (e == cudaSuccess) done.insert({key, dev});
+  return e;
+}
 
 struct PendingTiming {
   int kid;

@@ -22,7 +22,7 @@ struct MatchLayout {
   int64_t npad, ldm, m_off, tg_off, slot;
 };
 struct TepiLayout {
-  int64_t ldo, s_off, x_off, k_off, tg_off, tt_off, slot;
+  int64_t ldo, ar_off, ai_off, yr_off, yi_off, p_off, d_off, slot;
 };
 __host__ __device__ inline MatchLayout match_layout(int64_t nch) {
   MatchLayout L;
@@ -33,16 +33,30 @@ __host__ __device__ inline MatchLayout match_layout(int64_t nch) {
   L.slot = L.tg_off + 128 * 128 + 32;  // Tg: inverse of a 128 x 128 diagonal block
   return L;
 }
+// T epilogue (tepi.cu): five planes [nch][ldo] (Ar, Ai, Yr, Yi, P) and the vectors d (re, im), v
 __host__ __device__ inline TepiLayout tepi_layout(int64_t nch) {
   TepiLayout L;
-  L.ldo = (nch + 2) & ~1LL;  // >= nch + 1: room for the photoionisation right-hand side (column o)
-  L.s_off = 0;
-  L.x_off = nch * L.ldo + 32;
-  L.k_off = L.x_off + nch * L.ldo + 32;
-  L.tg_off = L.k_off + nch * L.ldo + 32;
-  L.tt_off = L.tg_off + 128 * 128 + 32;  // 128 x ldo scratch of the triangular inverse
-  L.slot = L.tt_off + 128 * L.ldo + 32;
+  L.ldo = (nch + 1) & ~1LL;  // even pitch (TMA stride rule)
+  const int64_t plane = nch * L.ldo + 32;
+  L.ar_off = 0;
+  L.ai_off = plane;
+  L.yr_off = 2 * plane;
+  L.yi_off = 3 * plane;
+  L.p_off = 4 * plane;
+  L.d_off = 5 * plane;
+  L.slot = L.d_off + ((3 * nch + 1) & ~1LL) + 32;
   return L;
+}
+
+// One-time per-device initialisation (rmx_api.cu): runs init() once per (key, current device),
+// serialised by a mutex; a failed init is retried on the next call. Kernel attributes and
+// __constant__ tables are per device, so a process-wide flag would skip them on a second device.
+cudaError_t once_per_device(const void *key, const std::function<cudaError_t()> &init);
+// cudaFuncAttributeMaxDynamicSharedMemorySize of `func` on the current device, set once
+inline cudaError_t ensure_smem_attr(const void *func, size_t bytes) {
+  return once_per_device(func, [&] {
+    return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  });
 }
 
 // rform.cu
@@ -60,7 +74,8 @@ bool encode_tmap_f64(CUtensorMap *map, const double *base, int64_t rows, int64_t
 constexpr int64_t kInt8Chunk = 8;  // minimum energies per INT8 chunk (rint8_chunk may take more)
 // below this many channels the 128 x 256 INT8 tiles and the conversion pass do not pay off (measured:
 // config small, nch 64: DMMA 3.2e5 E/s vs INT8 1.3e5 E/s; bp, nch 500: INT8 +30 %): R_INT8 falls back
-constexpr int64_t kInt8MinChannels = 256;  // energies per INT8-CRT pass (V planes: 16 nch nlev bytes each)
+// to the FP64 DMMA kernel
+constexpr int64_t kInt8MinChannels = 256;
 int64_t rint8_ldv(int64_t nlev);
 int64_t rint8_ldr(int64_t nch);
 int rint8_max_nlev();
@@ -94,8 +109,8 @@ struct LevelSums {
   double *omega = nullptr;
 };
 // Optional photoionisation output of the T epilogue (NEXT-1, photo.cu header): per energy
-//   v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) (j < o), y = (I + K_oo^2)^{-1} v (the Cholesky factor
-//   of the T route), M = y + i K_oo y, mabs2_j = |M_j|^2, sigma = C (E - E0) sum_j |M_j|^2.
+//   v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) (j < o), M = (I - i K_oo)^{-1} v (with the inverse the
+//   T route forms), mabs2_j = |M_j|^2, sigma = C (E - E0) sum_j |M_j|^2.
 // g == nullptr: off. g, Fp, Gp [ne][nch]; E [ne]; sigma [ne]; mabs2 [ne][nch] or nullptr.
 struct PhotoArgs {
   const double *g = nullptr, *Fp = nullptr, *Gp = nullptr, *E = nullptr;

@@ -1,11 +1,29 @@
 // tepi.cu - S5 of the sweep: T = 2i K_oo (I - i K_oo)^{-1} and |T_ij|^2 (BASELINE.json:5).
-// Real SPD route (reading T2): with K_oo symmetric,
-//   (I - iK)^{-1} = (I + iK)(I + K^2)^{-1}  =>  T = 2iX - 2KX,  X = (I + K K^T)^{-1} K
-// so Re T = -2P, Im T = 2X with P = K X, and |T_ij|^2 = 4 (X_ij^2 + P_ij^2). Per energy (one CTA,
-// persistent over energies): S = I + K K^T (lower, DMMA GEMM), blocked Cholesky S = L L^T, two
-// blocked triangular solves for X, P = K X (DMMA GEMM), then an epilogue pass writing |T|^2
-// (optional) and the row sums sum_j |T_ij|^2 in a fixed order (deterministic).
-// |T|^2 and the row sums are invariant under K -> -K, so the sweep may pass Y = -K directly.
+//
+// Route (reading T2). With A = I - iK_oo (complex symmetric, K_oo real symmetric by
+// reading M1), iK = I - A, so 2iK A^{-1} = 2(I - A) A^{-1} = 2(A^{-1} - I):
+//   T = 2 (A^{-1} - I),   |T_ij|^2 = 4 |(A^{-1})_ij - delta_ij|^2,
+// and only the inverse of A is needed. A's Hermitian part is I, so A has an LDL^T factorisation
+// without pivoting whose pivots satisfy Re d_j >= 1 (Schur complements of a matrix with Hermitian
+// part >= I keep Hermitian part >= I); the forward error of A^{-1} then grows like u ||K||, as for the
+// oracle's pivoted complex elimination - unlike the real SPD route through I + K^2 of round 1,
+// whose error grew like u ||K||^2 (1.5e-7 in |T|^2 at darc mesh 50169).
+//
+// Per energy (one CTA, persistent over energies, workspace slot = blockIdx.x); complex matrices are
+// two real planes (re, im) and every complex product is two real DMMA GEMMs whose k range covers
+// both halves (GemmArgs::nseg = 2):
+//   0. Ar = I, Ai = -K_oo
+//   1. blocked right-looking LDL^T, blocks of 64: the diagonal block is factored in shared memory
+//      together with the inverse of its unit-lower factor, Tinv_b = L_bb^{-1} (written over the
+//      block, D to a vector); W21 = A21 Tinv_b^T (= L21 D_b), L21 = W21 D_b^{-1}, and the trailing
+//      update A22 -= W21 L21^T (lower tiles)
+//   2. Z = L^{-1} in place, 128-row block rows: the 128 x 128 diagonal inverse from the two 64
+//      inverses, Z_{B,0:B} = -Tinv_B (L_{B,0:B} Z_{0:B,0:B})
+//   3. Y = D^{-1} Z
+//   4. A^{-1} = Z^T Y (lower tiles; Re into the P plane, Im in place over Y_i)
+//   5. mirror, |T_ij|^2 = 4 (Im^2 + (delta_ij - Re)^2), row sums in a fixed order (deterministic)
+// Executed flops ~ 4 o^3 (SURVEY §8(d) counts (16/3) o^3 as algorithmic).
+// |T|^2 and the row sums are invariant under K -> -K (A -> conj(A)).
 #include "cta_la.cuh"
 #include "rmx_internal.h"
 
@@ -13,14 +31,34 @@ namespace rmx {
 
 using namespace la;
 
+#ifdef RMX_PHASES
+// per-phase clock64 totals of block 0 (diagnostic build: python -m paper_1403_5524_b200.build --phases)
+__device__ unsigned long long g_tepi_phase[8];
+#define TPH_MARK(k)                                                         \
+  do {                                                                      \
+    __syncthreads();                                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      const unsigned long long now_ = clock64();                            \
+      g_tepi_phase[k] += now_ - ph_t0;                                      \
+      ph_t0 = now_;                                                         \
+    }                                                                       \
+  } while (0)
+#else
+#define TPH_MARK(k) \
+  do {              \
+  } while (0)
+#endif
+
+constexpr int CB = 64;          // block width of the complex LDL^T
+constexpr int CB_LD = CB + 1;   // smem pitch of the diagonal block
+
 struct TepiSmem {
-  union {  // the triangle scratch is only used between gemm calls
+  union {  // the diagonal-block scratch is only used between gemm calls
     double gemm[GEMM_SMEM_DOUBLES];
-    double tri[TRI_SMEM_DOUBLES];
+    double tri[2 * CB * CB_LD + 6 * CB];
   };
   GemmSync gs;
 };
-
 
 // P[j][i] = P[i][j] for j > i (upper triangle from the lower one), 32x32 blocks staged through
 // shared memory so that both the reads and the writes are coalesced row segments.
@@ -51,10 +89,96 @@ __device__ __forceinline__ void mirror_lower(double *P, int64_t ld, int o, doubl
   __syncthreads();
 }
 
-// Workspace slot: S (then P) [o][ldo], X [o][ldo], Kc [o][ldo] (aligned copy of K_oo),
-// Tg [32][32] (inverse of a 32x32 diagonal block of L: triangular solves run as DMMA GEMMs).
-// Factorisation / solves use outer blocks of NB = 64 (two inner 32-wide triangles) so that the
-// big updates run with K = 64.
+// LDL^T of the W x W (W <= 64) complex symmetric diagonal block A[p0.., p0..] (lower triangle of
+// the planes ar, ai) without pivoting, fused with the inverse of its unit-lower factor: in shared
+// memory row r holds X = L^{-1} in columns < c and the not yet eliminated part of A in columns
+// >= c, so elimination step c (X <- (I - l_c e_c^T) X, A22 -= l_c w_c^T) is one update of the
+// rows below c:  M[r][k] -= l_r u_k with u_k = X[c][k] (k < c) or A[k][c] (k > c), M[r][c] = -l_r.
+// On return the block holds Tinv = L^{-1} (unit lower, explicit zeros above the diagonal) and
+// d[p0 .. p0+W) the pivots (re, im). All NT threads.
+__device__ __noinline__ void diag_ldlt_inv(const MatView &ar, const MatView &ai, int p0, int W,
+                                           double *dr_out, double *di_out, double *sm) {
+  double *Mr = sm, *Mi = sm + CB * CB_LD;
+  double *lr = Mi + CB * CB_LD, *li = lr + CB, *ur = li + CB, *ui = ur + CB;
+  __syncthreads();
+  for (int q = threadIdx.x; q < W * CB; q += NT) {
+    const int r = q / CB, k = q % CB;
+    if (k <= r && k < W) {
+      Mr[r * CB_LD + k] = *ar.at(p0 + r, p0 + k);
+      Mi[r * CB_LD + k] = *ai.at(p0 + r, p0 + k);
+    }
+  }
+  for (int c = 0; c < W; ++c) {
+    __syncthreads();
+    const double dr = Mr[c * CB_LD + c], di = Mi[c * CB_LD + c];
+    const double den = fma(dr, dr, di * di);
+    const double ir = dr / den, ii = -di / den;  // 1/d (|d| >= Re d >= 1 in exact arithmetic)
+    for (int t = threadIdx.x; t < W; t += NT) {
+      if (t > c) {
+        const double xr = Mr[t * CB_LD + c], xi = Mi[t * CB_LD + c];
+        lr[t] = xr * ir - xi * ii;
+        li[t] = fma(xr, ii, xi * ir);
+        ur[t] = xr;
+        ui[t] = xi;
+      } else if (t < c) {
+        ur[t] = Mr[c * CB_LD + t];
+        ui[t] = Mi[c * CB_LD + t];
+      }
+    }
+    if (threadIdx.x == 0) {
+      dr_out[p0 + c] = dr;
+      di_out[p0 + c] = di;
+    }
+    __syncthreads();
+    const int nrow = W - c - 1;
+    for (int e = threadIdx.x; e < nrow * CB; e += NT) {
+      const int r = c + 1 + e / CB, k = e % CB;
+      if (k > r) continue;
+      const double a = lr[r], b = li[r];
+      if (k == c) {
+        Mr[r * CB_LD + c] = -a;
+        Mi[r * CB_LD + c] = -b;
+      } else {
+        const double xr = ur[k], xi = ui[k];
+        Mr[r * CB_LD + k] = fma(-a, xr, fma(b, xi, Mr[r * CB_LD + k]));
+        Mi[r * CB_LD + k] = fma(-a, xi, fma(-b, xr, Mi[r * CB_LD + k]));
+      }
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < W * W; q += NT) {
+    const int r = q / W, k = q % W;
+    *ar.at(p0 + r, p0 + k) = k < r ? Mr[r * CB_LD + k] : (k == r ? 1.0 : 0.0);
+    *ai.at(p0 + r, p0 + k) = k < r ? Mi[r * CB_LD + k] : 0.0;
+  }
+  __syncthreads();
+}
+
+// Complex product into the planes (cr, ci) at (r0, c0): C = alpha * (A.B) (set) or C -= A.B (sub),
+// A = (a_re, a_im), B = (b_re, b_im) given as operand pairs of one layout.
+__device__ __forceinline__ void cgemm(int M, int N, int K, const Op &are, const Op &aim, const Op &bre,
+                                      const Op &bim, const MatView &cr, const MatView &ci, int r0, int c0,
+                                      bool lower, bool sub, double alpha, int kband, double *smem,
+                                      GemmSync *gs) {
+  // Re = Ar.Br - Ai.Bi
+  GemmArgs g{are, bre, cr.at(r0, c0), cr.ld, M, N, K, lower, sub, false, 0.0, kband};
+  g.a2 = aim;
+  g.b2 = bim;
+  g.nseg = 2;
+  g.neg2 = true;
+  g.alpha = alpha;
+  gemm_rt(g, gemm_smem_align(smem), gs);
+  // Im = Ar.Bi + Ai.Br
+  g.b = bim;
+  g.b2 = bre;
+  g.neg2 = false;
+  g.C = ci.at(r0, c0);
+  g.ldc = ci.ld;
+  gemm_rt(g, gemm_smem_align(smem), gs);
+}
+
+// Workspace slot (tepi_layout): planes Ar, Ai (A, then L / Tinv blocks, then Z), Yr, Yi (scratch,
+// then Y = D^{-1} Z, then Im A^{-1} in place), P (Re A^{-1}); vectors d (re, im) and v.
 __global__ void __launch_bounds__(NT, 1)
     tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
                 const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
@@ -66,12 +190,12 @@ __global__ void __launch_bounds__(NT, 1)
   const int ldo = static_cast<int>(L.ldo);
   double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
   const CUtensorMap *vw = views + blockIdx.x * 5 * NVIEW;
-  const MatView Sv{vw + 0 * NVIEW, slot + L.s_off, ldo};
-  const MatView Xv{vw + 1 * NVIEW, slot + L.x_off, ldo};
-  const MatView Kv{vw + 2 * NVIEW, slot + L.k_off, ldo};
-  const MatView Tv{vw + 3 * NVIEW, slot + L.tg_off, TG};
-  const MatView Ttv{vw + 4 * NVIEW, slot + L.tt_off, ldo};
-  double *S = Sv.base;
+  const MatView Arv{vw + 0 * NVIEW, slot + L.ar_off, ldo};
+  const MatView Aiv{vw + 1 * NVIEW, slot + L.ai_off, ldo};
+  const MatView Yrv{vw + 2 * NVIEW, slot + L.yr_off, ldo};
+  const MatView Yiv{vw + 3 * NVIEW, slot + L.yi_off, ldo};
+  const MatView Pv{vw + 4 * NVIEW, slot + L.p_off, ldo};
+  double *dr = slot + L.d_off, *di = dr + n, *vv = di + n;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
 
@@ -85,105 +209,149 @@ __global__ void __launch_bounds__(NT, 1)
       if (ts >= 0) T2e = T2 + ts * static_cast<int64_t>(n) * n;
     }
     int bad = 0;
+#ifdef RMX_PHASES
+    unsigned long long ph_t0 = clock64();
+#endif
     if (o > 0) {
-      // Kc = K_oo (aligned, even pitch: operand of the TMA GEMM pipeline); X = 0 (Z = L^{-1} is
-      // built there, its strict upper part must stay zero)
+      if (pa.g) {
+        // NEXT-1 (10): v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) (j < o); gG_i staged in shared
+        // memory, i ascending
+        const double *ge = pa.g + e * n, *Fpe = pa.Fp + e * n, *Gpe = pa.Gp + e * n;
+        double *gG = sm.gemm;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += NT) gG[i] = ge[i] * Gpe[i];
+        __syncthreads();
+        for (int j = threadIdx.x; j < o; j += NT) {
+          double s = ge[j] * Fpe[j];
+          for (int i = 0; i < n; ++i) s = fma(gG[i], Ke[static_cast<int64_t>(i) * ldk + j], s);
+          vv[j] = 0.5 * s;
+        }
+      }
+      // 0. Ar = I, Ai = -K_oo
       for (int i = warp_id(); i < o; i += NW) {
         const double *src = Ke + static_cast<int64_t>(i) * ldk;
-        double *dk = Kv.at(i, 0), *dx = Xv.at(i, 0);
+        double *pr = Arv.at(i, 0), *pi = Aiv.at(i, 0);
         constexpr int U = 8;  // 8 independent loads in flight per lane
         for (int j0 = lane_id(); j0 < o; j0 += 32 * U) {
           double v[U];
 #pragma unroll
           for (int q = 0; q < U; ++q) v[q] = (j0 + 32 * q < o) ? src[j0 + 32 * q] : 0.0;
 #pragma unroll
-          for (int q = 0; q < U; ++q)
-            if (j0 + 32 * q < o) {
-              dk[j0 + 32 * q] = v[q];
-              dx[j0 + 32 * q] = 0.0;
+          for (int q = 0; q < U; ++q) {
+            const int j = j0 + 32 * q;
+            if (j < o) {
+              pi[j] = -v[q];
+              pr[j] = (i == j) ? 1.0 : 0.0;
             }
+          }
         }
       }
-      if (pa.g) {
-        // NEXT-1 (10): v_j = (1/2)(g_j F'_j + sum_i g_i G'_i K_ij) into Kc column o; gG_i staged in
-        // shared memory, i ascending
-        const double *ge = pa.g + e * n, *Fpe = pa.Fp + e * n, *Gpe = pa.Gp + e * n;
-        double *gG = sm.gemm;
-        for (int i = threadIdx.x; i < n; i += NT) gG[i] = ge[i] * Gpe[i];
-        __syncthreads();
-        for (int j = threadIdx.x; j < o; j += NT) {
-          double s = ge[j] * Fpe[j];
-          for (int i = 0; i < n; ++i) s = fma(gG[i], Ke[static_cast<int64_t>(i) * ldk + j], s);
-          *Kv.at(j, o) = 0.5 * s;
+      TPH_MARK(0);  // copy (+ photo v)
+      // 1. blocked LDL^T
+      for (int P0 = 0; P0 < o; P0 += CB) {
+        const int W = min(CB, o - P0), m = o - P0 - W;
+        diag_ldlt_inv(Arv, Aiv, P0, W, dr, di, sm.tri);
+        TPH_MARK(1);  // diagonal blocks
+        if (m > 0) {
+          // W21 = A21 Tinv^T -> Y planes [0, m) x [0, W)
+          cgemm(m, W, W, opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0), opk(Arv, P0, P0), opk(Aiv, P0, P0),
+                Yrv, Yiv, 0, 0, false, false, 1.0, 0, smg, gs);
+          TPH_MARK(2);  // W21 = A21 Tinv^T
+          // L21 = W21 D^{-1} over A21
+          double *idr = sm.tri, *idi = sm.tri + CB;
+          for (int j = threadIdx.x; j < W; j += NT) {
+            const double a = dr[P0 + j], b = di[P0 + j], den = fma(a, a, b * b);
+            idr[j] = a / den;
+            idi[j] = -b / den;
+          }
+          __syncthreads();
+          for (int q = threadIdx.x; q < m * CB; q += NT) {
+            const int i = q / CB, j = q % CB;
+            if (j < W) {
+              const double xr = *Yrv.at(i, j), xi = *Yiv.at(i, j);
+              *Arv.at(P0 + W + i, P0 + j) = xr * idr[j] - xi * idi[j];
+              *Aiv.at(P0 + W + i, P0 + j) = fma(xr, idi[j], xi * idr[j]);
+            }
+          }
+          TPH_MARK(3);  // L21 scaling
+          // A22 -= W21 L21^T (lower tiles)
+          cgemm(m, m, W, opk(Yrv, 0, 0), opk(Yiv, 0, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0),
+                Arv, Aiv, P0 + W, P0 + W, true, true, 1.0, 0, smg, gs);
+          TPH_MARK(4);  // trailing updates
         }
       }
-      __syncthreads();
-      // S = I + K_oo K_oo^T (lower tiles)
-      gemm_set(o, o, o, opk(Kv, 0, 0), opk(Kv, 0, 0), Sv, 0, 0, true, 1.0, smg, gs);
-      // blocked Cholesky S = L L^T (lower), 128-wide blocks: diagonal block in smem, then
-      // L21 = S21 L11^{-T} as one in-place GEMM with the explicit inverse, then the K = 128 update
-      for (int P0 = 0; P0 < o; P0 += NB) {
-        const int W = min(NB, o - P0);
-        bad |= chol_diag_blk(S, ldo, P0, W, sm.tri);
-        if (P0 + W < o) {
-          tri_inv128(Sv, P0, W, TRI_LOWER, Tv, smg, gs);
-          // L21^T = L11^{-1} S21^T (stored transposed, in place): one 128-row tile row, so each
-          // output tile depends only on its own rows of S21
-          gemm_set_t(W, o - P0 - W, W, opk(Tv, 0, 0), opk(Sv, P0 + W, P0), Sv, P0 + W, P0, smg, gs);
-          const int m2 = o - P0 - W;
-          gemm_sub(m2, m2, W, opk(Sv, P0 + W, P0), opk(Sv, P0 + W, P0), Sv, P0 + W, P0 + W, true,
-                   smg, gs);
+      // 2. Z = L^{-1} in place, 128-row block rows
+      for (int R0 = 0; R0 < o; R0 += 2 * CB) {
+        const int W = min(2 * CB, o - R0), W2 = W - CB;
+        if (W2 > 0) {
+          // the upper-right 64-block of the diagonal 128-block is zero in Tinv_128 (the trailing
+          // updates of step 1 left values there: their lower tiles overhang the diagonal)
+          for (int q = threadIdx.x; q < CB * W2; q += NT) {
+            *Arv.at(R0 + q / W2, R0 + CB + q % W2) = 0.0;
+            *Aiv.at(R0 + q / W2, R0 + CB + q % W2) = 0.0;
+          }
+          // Tinv_128 = [[T1, 0], [-T2 L21 T1, T2]]: Q1 = L21 T1 -> Y, then -T2 Q1 over L21
+          cgemm(W2, CB, CB, opk(Arv, R0 + CB, R0), opk(Aiv, R0 + CB, R0), opn(Arv, R0, R0), opn(Aiv, R0, R0),
+                Yrv, Yiv, 0, 0, false, false, 1.0, 0, smg, gs);
+          cgemm(W2, CB, W2, opk(Arv, R0 + CB, R0 + CB), opk(Aiv, R0 + CB, R0 + CB), opn(Yrv, 0, 0),
+                opn(Yiv, 0, 0), Arv, Aiv, R0 + CB, R0, false, false, -1.0, 0, smg, gs);
         }
-      }
-      // Z = L^{-1} (lower, in X) block row by block row:  Z_bb = L_bb^{-1} (128 x 128 inverse),
-      // Z_{b,0:b} = -Z_bb (L_{b,0:b} Z_{0:b,0:b}); the triangular factor Z of the product skips its
-      // zero k slices (kband 2), so the step costs (1/3) o^3 in total
-      for (int R0 = 0; R0 < o; R0 += NB) {
-        const int W = min(NB, o - R0);
-        tri_inv128(Sv, R0, W, TRI_LOWER, Tv, smg, gs);
         if (R0 > 0) {
-          gemm_set_kb(W, R0, R0, opk(Sv, R0, 0), opn(Xv, 0, 0), Ttv, 0, 0, false, 2, smg, gs);
-          gemm_sub(W, R0, W, opk(Tv, 0, 0), opn(Ttv, 0, 0), Xv, R0, 0, false, smg, gs);
-        }
-        for (int q = threadIdx.x; q < W * W; q += NT) {
-          const int r = q / W, cc = q % W;
-          *Xv.at(R0 + r, R0 + cc) = Tv.base[r * TG + cc];  // upper part of Tv is zero
-        }
-        __syncthreads();
-      }
-      // S^{-1} = Z^T Z (lower tiles, kband 1: Z(k, i) = 0 for k < i), over L, then mirrored
-      gemm_set_kb(o, o, o, opn(Xv, 0, 0), opn(Xv, 0, 0), Sv, 0, 0, true, 1, smg, gs);
-      mirror_lower(S, ldo, o, sm.gemm);
-      // X = S^{-1} K_oo = (I + K^2)^{-1} K: symmetric (K_oo symmetric, reading M1), lower tiles then
-      // mirrored; overwrites Z
-      gemm_set(o, o, o, opk(Sv, 0, 0), opn(Kv, 0, 0), Xv, 0, 0, true, 0.0, smg, gs);
-      mirror_lower(Xv.base, ldo, o, sm.gemm);
-      if (pa.g) {
-        // NEXT-1 (11): y = S^{-1} v into X column o (v in Kc column o)
-        double *vs = sm.gemm;
-        for (int j = threadIdx.x; j < o; j += NT) vs[j] = *Kv.at(j, o);
-        __syncthreads();
-        for (int i = warp_id(); i < o; i += NW) {
-          const double *sr = Sv.at(i, 0);
-          double t = 0.0;
-          for (int j = lane_id(); j < o; j += 32) t = fma(sr[j], vs[j], t);
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-          if (lane_id() == 0) *Xv.at(i, o) = t;
+          // Tt = L_{B,0:R0} Z_{0:R0,0:R0} -> Y (Z lower triangular: kband 2); Z_B = -Tinv_128 Tt
+          cgemm(W, R0, R0, opk(Arv, R0, 0), opk(Aiv, R0, 0), opn(Arv, 0, 0), opn(Aiv, 0, 0), Yrv, Yiv, 0, 0,
+                false, false, 1.0, 2, smg, gs);
+          cgemm(W, R0, W, opk(Arv, R0, R0), opk(Aiv, R0, R0), opn(Yrv, 0, 0), opn(Yiv, 0, 0), Arv, Aiv, R0,
+                0, false, false, -1.0, 0, smg, gs);
         }
       }
-      // P = K_oo X = K S^{-1} K = I - S^{-1} (K and S commute): in place of S^{-1}
-      __syncthreads();
+      TPH_MARK(5);  // Z = L^{-1}
+      // 3. Y = D^{-1} Z (zeros above the diagonal); Z's strict upper part inside its 128 x 128
+      // diagonal blocks is zeroed too (both are read as explicit zeros by the k-band GEMM below)
       for (int i = warp_id(); i < o; i += NW) {
-        double *pr = Sv.at(i, 0);
-        for (int j = lane_id(); j < o; j += 32) pr[j] = (i == j ? 1.0 : 0.0) - pr[j];
+        const double a = dr[i], b = di[i], den = fma(a, a, b * b);
+        const double ir = a / den, ii = -b / den;
+        double *zr = Arv.at(i, 0), *zi = Aiv.at(i, 0), *yr = Yrv.at(i, 0), *yi = Yiv.at(i, 0);
+        const int zend = min(o, (i / (2 * CB) + 1) * (2 * CB));
+        for (int j = lane_id(); j < o; j += 32) {
+          if (j <= i) {
+            const double xr = zr[j], xi = zi[j];
+            yr[j] = xr * ir - xi * ii;
+            yi[j] = fma(xr, ii, xi * ir);
+          } else {
+            yr[j] = 0.0;
+            yi[j] = 0.0;
+            if (j < zend) {
+              zr[j] = 0.0;
+              zi[j] = 0.0;
+            }
+          }
+        }
       }
-      __syncthreads();
+      // 4. A^{-1} = Z^T Y (lower tiles; A(i,k) = Z(k,i) = 0 for k < i: kband 1). Re -> P, then Im
+      // in place over Y_i: an output tile is stored after its own reads, and later tiles read only
+      // rows >= their first row or other columns (row-major tile order).
+      {
+        GemmArgs g{opn(Arv, 0, 0), opn(Yrv, 0, 0), Pv.base, Pv.ld, o, o, o, true, false, false, 0.0, 1};
+        g.a2 = opn(Aiv, 0, 0);
+        g.b2 = opn(Yiv, 0, 0);
+        g.nseg = 2;
+        g.neg2 = true;
+        gemm_rt(g, gemm_smem_align(smg), gs);
+        g.b = opn(Yiv, 0, 0);
+        g.b2 = opn(Yrv, 0, 0);
+        g.neg2 = false;
+        g.C = Yiv.base;
+        gemm_rt(g, gemm_smem_align(smg), gs);
+      }
+      TPH_MARK(6);  // Y = D^{-1} Z and A^{-1} = Z^T Y
+      // 5. symmetric A^{-1}: upper triangles from the lower ones
+      mirror_lower(Pv.base, ldo, o, sm.gemm);
+      mirror_lower(Yiv.base, ldo, o, sm.gemm);
     }
-    // epilogue: |T|^2 = 4 (X^2 + P^2), row sums in fixed order
+    // epilogue: |T|^2 = 4 (Im^2 + (delta - Re)^2), row sums in fixed order
     for (int i = warp_id(); i < n; i += NW) {
       double s = 0.0;
-      const double *xr = Xv.at(i, 0), *pr = Sv.at(i, 0);
+      const double *xr = Yiv.at(i, 0), *pr = Pv.at(i, 0);
       constexpr int U = 4;  // 2U independent loads in flight per lane
       for (int j0 = lane_id(); j0 < n; j0 += 32 * U) {
         double xv[U], pv[U];
@@ -192,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1)
           const int j = j0 + 32 * q;
           const bool in = i < o && j < o;
           xv[q] = in ? xr[j] : 0.0;
-          pv[q] = in ? pr[j] : 0.0;
+          pv[q] = in ? (i == j ? 1.0 : 0.0) - pr[j] : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < U; ++q) {
@@ -210,22 +378,28 @@ __global__ void __launch_bounds__(NT, 1)
       if (rowsum && lane_id() == 0) rowsum[e * n + i] = s;
     }
     if (pa.g) {
-      // NEXT-1 (11)-(12): y = X[:, o] = (I + K_oo^2)^{-1} v; M = y + i K_oo y; |M_j|^2; sigma.
+      // NEXT-1 (11)-(12): M = A^{-1} v = (Re A^{-1}) v + i (Im A^{-1}) v; |M_j|^2; sigma.
       // Row sums in a fixed order: warp w takes rows w, w + NW, ...; warps combined in order.
-      double *ys = sm.gemm, *wsum = sm.gemm + n + 1;
+      double *vs = sm.gemm, *wsum = sm.gemm + n + 1;
       __syncthreads();
-      for (int j = threadIdx.x; j < o; j += NT) ys[j] = *Xv.at(j, o);
+      for (int j = threadIdx.x; j < o; j += NT) vs[j] = vv[j];
       __syncthreads();
       double part = 0.0;
       for (int i = warp_id(); i < n; i += NW) {
         double m2 = 0.0;
         if (i < o) {
-          const double *kr = Kv.at(i, 0);
-          double t = 0.0;
-          for (int j = lane_id(); j < o; j += 32) t = fma(kr[j], ys[j], t);
+          const double *pr = Pv.at(i, 0), *xr = Yiv.at(i, 0);
+          double tr = 0.0, ti = 0.0;
+          for (int j = lane_id(); j < o; j += 32) {
+            tr = fma(pr[j], vs[j], tr);
+            ti = fma(xr[j], vs[j], ti);
+          }
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-          m2 = fma(ys[i], ys[i], t * t);
+          for (int off = 16; off > 0; off >>= 1) {
+            tr += __shfl_xor_sync(0xffffffffu, tr, off);
+            ti += __shfl_xor_sync(0xffffffffu, ti, off);
+          }
+          m2 = fma(tr, tr, ti * ti);
         }
         if (!isfinite(m2)) bad = 1;
         if (pa.mabs2 && lane_id() == 0) pa.mabs2[e * n + i] = m2;
@@ -254,8 +428,11 @@ __global__ void __launch_bounds__(NT, 1)
           const int j0 = lv.level_start[lb], j1 = lv.level_start[lb + 1];
           double acc = 0.0;
           for (int i = i0; i < i1; ++i) {
-            const double *xr = Xv.at(i, 0), *pr = Sv.at(i, 0);
-            for (int j = j0; j < j1; ++j) acc += 4.0 * fma(xr[j], xr[j], pr[j] * pr[j]);
+            const double *xr = Yiv.at(i, 0), *pr = Pv.at(i, 0);
+            for (int j = j0; j < j1; ++j) {
+              const double p = (i == j ? 1.0 : 0.0) - pr[j];
+              acc += 4.0 * fma(xr[j], xr[j], p * p);
+            }
           }
           Om[static_cast<int64_t>(la) * lv.nlevel + lb] += lv.g * acc;
         }
@@ -263,30 +440,33 @@ __global__ void __launch_bounds__(NT, 1)
     }
     bad = __syncthreads_or(bad);
     if (bad && threadIdx.x == 0) set_status(status, e, RMX_E_NONFINITE);
+    TPH_MARK(7);  // mirror + epilogue (+ photo, levels)
   }
 }
 
+#ifdef RMX_PHASES
+extern "C" int rmx_debug_tepi_phases(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_tepi_phase, sizeof(g_tepi_phase)));
+}
+#endif
+
 int64_t tepi_ws_doubles_per_slot(int64_t nch) { return tepi_layout(nch).slot; }
 
-// Matrices of one slot whose TMA descriptors the kernel uses: (S, X, Kc, Tg, Tt), NVIEW boxes each.
+// Matrices of one slot whose TMA descriptors the kernel uses: (Ar, Ai, Yr, Yi, P), NVIEW boxes each.
 void tepi_view_specs(int64_t nch, std::vector<MatSpec> &specs) {
   const TepiLayout L = tepi_layout(nch);
-  specs = {MatSpec{L.s_off, nch, L.ldo, L.ldo}, MatSpec{L.x_off, nch, L.ldo, L.ldo},
-           MatSpec{L.k_off, nch, L.ldo, L.ldo}, MatSpec{L.tg_off, TG, TG, TG},
-           MatSpec{L.tt_off, NB, L.ldo, L.ldo}};
+  specs = {MatSpec{L.ar_off, nch, L.ldo, L.ldo}, MatSpec{L.ai_off, nch, L.ldo, L.ldo},
+           MatSpec{L.yr_off, nch, L.ldo, L.ldo}, MatSpec{L.yi_off, nch, L.ldo, L.ldo},
+           MatSpec{L.p_off, nch, L.ldo, L.ldo}};
 }
 
 cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t nch, int64_t ne,
                         const int32_t *n_open, double *T2, const int64_t *t2_slot, double *rowsum,
                         const LevelSums &lv, const PhotoArgs &pa, double *ws, int64_t ws_slot,
                         const CUtensorMap *views, int64_t ws_slots, int32_t *status, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t ce = cudaFuncSetAttribute(tepi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sizeof(TepiSmem)));
-    if (ce != cudaSuccess) return ce;
-    attr = true;
-  }
+  cudaError_t ce = ensure_smem_attr(reinterpret_cast<const void *>(tepi_kernel), sizeof(TepiSmem));
+  if (ce != cudaSuccess) return ce;
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
   tepi_kernel<<<grid, NT, sizeof(TepiSmem), st>>>(K, ldk, kstride, static_cast<int>(nch), ne, n_open,
                                                   T2, t2_slot, rowsum, lv, pa, ws, ws_slot, views, status);

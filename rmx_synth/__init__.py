@@ -282,3 +282,62 @@ def symmetry_cases(nsym: int, nlevel: int, seed: int, nlev: int = 300, ne: int =
         ls = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32)
         out.append((case, ls))
     return lev, E, out
+
+
+def isolated_poles(case: Case, n: int, lo: float, hi: float, min_gap: float) -> np.ndarray:
+    """Up to n poles E_k inside [lo, hi] whose nearest neighbouring pole is >= min_gap away, spread
+    evenly over the candidates (input structure only)."""
+    Ek = case.Ek
+    gaps = np.minimum(np.diff(Ek, prepend=-np.inf), np.diff(Ek, append=np.inf))
+    cand = Ek[(Ek > lo) & (Ek < hi) & (gaps >= min_gap)]
+    if len(cand) == 0:
+        return cand
+    return cand[np.unique(np.linspace(0, len(cand) - 1, min(n, len(cand))).round().astype(int))]
+
+
+def survey_sample(case: Case):
+    """The darc / fine parity samples of SURVEY.md §8(d) (the energies the oracle is timed and compared
+    on), as energies with labels. darc (16): 4 isolated poles at offsets -1e-3, -1e-5, +1e-5; the
+    three mesh points next to a pole of K found in round 1 (mesh 50106, 50169, 50228: ||K_oo|| up to
+    3e5); one energy 1e-4 above a threshold. fine (32): 4 window resonances (narrow poles,
+    |w| ~ 1e-3) at offsets +1.5e-6, -1e-5, +1e-4; 2 background poles inside the window at -1e-5, +1e-5;
+    4 energies 1e-4 above a threshold; 12 evenly spaced mesh points. Returns (E [n], labels [n])."""
+    E, lab = [], []
+    if case.name == "darc":
+        lo, hi = case.E[0], case.E[-1]
+        for p in isolated_poles(case, 4, lo + 1.0, hi - 1.0, 3e-3):
+            for off in (-1e-3, -1e-5, 1e-5):
+                E.append(p + off)
+                lab.append(f"pole {p:.6f} {off:+.0e}")
+        for m in (50106, 50169, 50228):
+            E.append(case.E[m])
+            lab.append(f"mesh {m} (K pole)")
+        th = np.unique(case.eps[(case.eps > lo) & (case.eps < hi)])
+        t = th[len(th) // 2]
+        E.append(t + 1e-4)
+        lab.append(f"threshold {t:.6f} +1e-4")
+    elif case.name == "fine":
+        lo, hi = case.E[0], case.E[-1]
+        win = isolated_poles(case, 10 ** 6, lo + 1e-3, hi - 1e-3, 2e-4)
+        # resonance poles: the narrow ones (column norm ~ 1e-3 sqrt(nch)); background poles: wide
+        cn = {float(p): float(np.linalg.norm(case.w[:, int(np.searchsorted(case.Ek, p))])) for p in win}
+        res = np.array([p for p in win if cn[float(p)] < 0.2])
+        bg = np.array([p for p in win if cn[float(p)] >= 0.2])
+        for p in res[np.linspace(0, len(res) - 1, 4).round().astype(int)]:
+            for off in (1.5e-6, -1e-5, 1e-4):
+                E.append(p + off)
+                lab.append(f"resonance {p:.7f} {off:+.1e}")
+        for p in bg[np.linspace(0, len(bg) - 1, 2).round().astype(int)]:
+            for off in (-1e-5, 1e-5):
+                E.append(p + off)
+                lab.append(f"background pole {p:.7f} {off:+.0e}")
+        th = np.unique(case.eps[(case.eps > lo) & (case.eps < hi - 1e-3)])
+        for t in th[np.linspace(0, len(th) - 1, 4).round().astype(int)]:
+            E.append(t + 1e-4)
+            lab.append(f"threshold {t:.7f} +1e-4")
+        for m in np.linspace(0, case.ne - 1, 12).round().astype(int):
+            E.append(case.E[m])
+            lab.append(f"mesh {m}")
+    else:
+        raise KeyError(case.name)
+    return np.array(E, dtype=np.float64), lab

@@ -124,18 +124,17 @@ def test_int8_darc_block(ctx):
         assert np.max(np.abs(R8[ii, jj] - vals)) / np.max(np.abs(R8)) < 1e-12
         o = int(no[l])
         assert nrel(out8["T2"][d].cpu().numpy(), out64["T2"][d].cpu().numpy()) < 1e-8
-    # row sums of all 296 energies: INT8 and DMMA R agree to the |T|^2 bar except where the matching is
-    # ill-conditioned; there both are as far from the oracle (the R rounding of either path is
-    # amplified the same way), which is checked at the worst energy
+    # row sums of all 296 energies: INT8 and DMMA R give the same |T|^2 row sums to the 1e-8 bar; the
+    # three energies where they differ most are compared with the oracle, hard 1e-8 bar, both paths
     rs8, rs64 = out8["rowsum"].cpu().numpy(), out64["rowsum"].cpu().numpy()
     per = np.max(np.abs(rs8 - rs64), axis=1) / np.max(np.abs(rs64), axis=1)
-    assert np.median(per) < 1e-10 and np.sum(per > 1e-8) <= 0.05 * len(E), np.sort(per)[-5:]
-    l = int(np.argmax(per))
-    if per[l] > 1e-8:
-        ref = oracle.sweep(c.w, c.Ek, c.a, E[l:l + 1], F[l:l + 1], G[l:l + 1], Fp[l:l + 1], Gp[l:l + 1],
-                           no[l:l + 1], np.arange(1), want=("rowsum",))["rowsum"][0]
-        e8, e64 = nrel(rs8[l], ref), nrel(rs64[l], ref)
-        assert e8 <= 2.0 * e64 + 1e-9, (l, e8, e64)
+    assert np.max(per) < 1e-8, np.sort(per)[-5:]
+    worst = [int(x) for x in np.argsort(per)[-3:]]
+    ref = oracle.sweep(c.w, c.Ek, c.a, E, F, G, Fp, Gp, no, np.array(worst), want=("rowsum",),
+                       threads=oracle.default_threads())["rowsum"]
+    for q, l in enumerate(worst):
+        e8, e64 = nrel(rs8[l], ref[q]), nrel(rs64[l], ref[q])
+        assert e8 < 1e-8 and e64 < 1e-8, (l, e8, e64)
 
 
 def test_int8_many_poles_signed_residues(ctx):

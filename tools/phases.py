@@ -28,3 +28,11 @@ names = ["formation", "panels (panel_lu + K=32 updates)", "U12 + K=128 trailing"
 tot = sum(out[k] for k in range(7))
 for k, n in enumerate(names):
     print(f"{n:36s} {out[k] / 1e6:10.1f} Mcycles {100 * out[k] / tot:5.1f} %")
+# T epilogue (tepi.cu, complex LDL^T route)
+ctx.lib.rmx_debug_tepi_phases(out)
+names = ["copy (+ photo v)", "diagonal LDL^T + inverse (smem)", "W21 = A21 Tinv^T", "L21 scaling",
+         "trailing updates (K = 2 x 64)", "Z = L^-1", "Y = D^-1 Z, A^-1 = Z^T Y", "mirror + epilogue"]
+tot = sum(out[k] for k in range(8))
+print()
+for k, n in enumerate(names):
+    print(f"tepi {n:36s} {out[k] / 1e6:10.1f} Mcycles {100 * out[k] / tot:5.1f} %")
