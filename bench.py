@@ -188,9 +188,33 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on this node, 127.0.0.1 rendezvous; refuse if fewer GPUs are visible."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if args.gpus > have:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible; "
+              f"refusing to run {args.gpus} ranks", file=sys.stderr, flush=True)
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     rank, world, local = rdist.env_rank_world()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -199,28 +223,33 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         rdist.init_process_group("nccl")
+        print(f"[bench rank {rank}] NCCL communicator: {torch.distributed.get_world_size()} ranks, "
+              f"backend {torch.distributed.get_backend()}, device cuda:{local}", file=sys.stderr, flush=True)
     dev = torch.device(f"cuda:{local}")
     cfg = syn.CONFIGS[args.config]
     nch, nlev = cfg["nch"], cfg["nlev"]
 
-    # ---- inputs: rank 0 generates W/E_k (seeded), broadcast to the other ranks
+    # ---- inputs: rank 0 generates the case (seeded); the other ranks generate nothing and receive
+    # W, E_k, the thresholds and the mesh by broadcast (PAPER.md:208-211 root read + MPI_BCAST)
     t_setup = time.perf_counter()
-    case = syn.make_case(args.config) if rank == 0 or world == 1 else None
     ldw = nlev + (nlev & 1)
-    w_d = torch.zeros((nch, ldw), dtype=torch.float64, device=dev)
-    Ek_d = torch.empty(nlev, dtype=torch.float64, device=dev)
-    if case is not None:
+    if world == 1:
+        case = syn.make_case(args.config)
+        w_d = torch.zeros((nch, ldw), dtype=torch.float64, device=dev)
         w_d[:, :nlev] = torch.from_numpy(case.w).to(dev)
-        Ek_d.copy_(torch.from_numpy(case.Ek))
-    if world > 1:
-        rdist.broadcast_inputs([w_d, Ek_d])
-        meta = syn.make_case.__name__  # mesh/thresholds are cheap and seeded: recomputed locally
-        if case is None:
-            case = syn.make_case(args.config)  # thresholds + mesh (W/Ek above come from the broadcast)
+        Ek_d = torch.from_numpy(case.Ek).to(dev)
+        eps, E_mesh, a = case.eps, case.E, case.a
+    else:
+        torch.cuda.synchronize()
+        b0 = time.perf_counter()
+        w_d, Ek_d, eps_d, E_d, a = rdist.broadcast_case(syn.make_case(args.config) if rank == 0 else None, dev)
+        torch.cuda.synchronize()
+        bcast_s = time.perf_counter() - b0
+        eps, E_mesh = eps_d.cpu().numpy(), E_d.cpu().numpy()
     ctx = rmx.Context(local)
     if args.r_algo == "int8":
         ctx.set_r_algo(rmx.R_INT8)
-    ne = case.ne
+    ne = len(E_mesh)
     batch = args.batch if args.batch > 0 else 2 * torch.cuda.get_device_properties(dev).multi_processor_count
     if args.config in ("tiny", "small") and args.batch <= 0:
         batch = min(ne, 4096 if args.config == "small" else ne)
@@ -236,9 +265,9 @@ def main():
     step_inputs = []
     for s in range(nsteps):
         lo, hi = rdist.block_range(block_of_step(s), ne, batch)
-        E = case.E[lo:hi]
-        F, G, Fp, Gp = syn.asymptotic(case.eps, E, case.a)
-        no = syn.n_open(case.eps, E)
+        E = E_mesh[lo:hi]
+        F, G, Fp, Gp = syn.asymptotic(eps, E, a)
+        no = syn.n_open(eps, E)
         step_inputs.append(dict(
             E=torch.from_numpy(E).to(dev), F=torch.from_numpy(F).to(dev), G=torch.from_numpy(G).to(dev),
             Fp=torch.from_numpy(Fp).to(dev), Gp=torch.from_numpy(Gp).to(dev),
@@ -247,8 +276,19 @@ def main():
 
     def one_step(s):
         d = step_inputs[s]
-        return ctx.sweep(w_d, Ek_d, case.a, d["E"], d["F"], d["G"], d["Fp"], d["Gp"], d["no"],
+        return ctx.sweep(w_d, Ek_d, a, d["E"], d["F"], d["G"], d["Fp"], d["Gp"], d["no"],
                          batch=batch, prepared=(nlev, ldw))
+
+    # mesh indices each rank processes in the timed region (same block_of_step rule on every rank)
+    def timed_shards():
+        out = []
+        for r in range(world):
+            blocks = rdist.cyclic_blocks(ne, batch, world, r)
+            idx = [np.arange(*rdist.block_range(blocks[min(len(blocks) - 1, int((s + 0.5) * len(blocks) / nsteps))],
+                                                ne, batch)) for s in range(args.warmup, nsteps)]
+            out.append(np.concatenate(idx))
+        return out
+    shards = timed_shards() if world > 1 else None
 
     # ---- device-resident timed region -------------------------------------------------------
     for s in range(args.warmup):
@@ -261,11 +301,16 @@ def main():
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     outs = []
+    full = None
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for s in range(args.warmup, nsteps):
             outs.append(one_step(s))
+        if world > 1:
+            # S6: one all-gather of the per-energy row sums, reassembled in mesh order on every rank,
+            # inside the timed wall (first batch launch to gather completion)
+            full = rdist.gather_summaries(torch.cat([o["rowsum"] for o in outs]), ne, batch, world, shards)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -316,18 +361,16 @@ def main():
     path_tflops = (fr + fk + ft) / (ms / 1e3) / 1e12
     ms_g, n_g = stats.get("i8gemm", (0.0, 0))
 
-    # ---- results gather (one all-gather, outside the timed region) ---------------------------
-    gather_ms = None
+    # ---- the gathered result is complete and consistent on every rank -------------------------
+    gather = None
     if world > 1:
-        loc = torch.cat([o["rowsum"] for o in outs])
-        torch.cuda.synchronize()
-        g0 = time.perf_counter()
-        pad = torch.zeros((args.steps * batch, nch), dtype=torch.float64, device=dev)
-        pad[: loc.shape[0]] = loc
-        full = torch.empty((world * args.steps * batch, nch), dtype=torch.float64, device=dev)
-        torch.distributed.all_gather_into_tensor(full, pad)
-        torch.cuda.synchronize()
-        gather_ms = 1e3 * (time.perf_counter() - g0)
+        mine = torch.cat([o["rowsum"] for o in outs])
+        idx = torch.from_numpy(shards[rank]).to(dev)
+        assert torch.equal(full[idx], mine)
+        covered = np.concatenate(shards)
+        gather = {"energies": int(len(covered)), "bytes": int(len(covered) * nch * 8),
+                  "inside_timed_region": True, "w_broadcast_s": round(bcast_s, 3),
+                  "w_broadcast_bytes": int(w_d.numel() * 8)}
 
     # ---- end-to-end through the C ABI with host buffers ---------------------------------------
     e2e = None
@@ -353,7 +396,7 @@ def main():
 
         def host_step(s):
             h = host_steps[s]
-            return ctx.sweep_host(w_h, Ek_h, case.a, h["E"], h["F"], h["G"], h["Fp"], h["Gp"], h["no"],
+            return ctx.sweep_host(w_h, Ek_h, a, h["E"], h["F"], h["G"], h["Fp"], h["Gp"], h["no"],
                                   batch=batch, rowsum=h["rowsum"], status=h["status"])
 
         for s in range(args.warmup):
@@ -383,6 +426,7 @@ def main():
     # ---- CPU oracle baseline (rank 0, N = 1 only) --------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # (world == 1: rank 0 holds the generated case)
         sample = [case.ne // 2 + s for s in range(max(1, args.oracle_sample))]
         if args.config in ("tiny", "small"):
             sample = list(range(0, case.ne, max(1, case.ne // 256)))
@@ -450,7 +494,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "setup_s": round(setup_s, 2),
-            "gather_ms": gather_ms,
+            "gather": gather,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

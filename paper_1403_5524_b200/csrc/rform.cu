@@ -149,7 +149,7 @@ __device__ __forceinline__ void rform_slab(double (&acc)[2][4][4][2], uint32_t a
 template <class C>
 __device__ __forceinline__ void rform_fill(uint8_t *smem, const CUtensorMap *wmap,
                                            const double *__restrict__ Ek, double Ee, int nlev,
-                                           int kt, bool diag, int ti, int tj) {
+                                           int kt, bool diag, int ti, int tj, int kstar) {
   double *dsm = reinterpret_cast<double *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
   uint64_t *empty = full + C::STAGES;
@@ -160,7 +160,7 @@ __device__ __forceinline__ void rform_fill(uint8_t *smem, const CUtensorMap *wma
   if (k < nlev) {
     const double diff = __ldg(Ek + k) - Ee;
     if (fabs(diff) < kPoleGuard) *pole_flag = 1;
-    dv = 1.0 / diff;
+    dv = (k == kstar) ? 0.0 : 1.0 / diff;  // the nearest pole's term is added in the epilogue
   }
   dsm[s * C::BK + lane] = dv;
   __syncwarp();
@@ -186,7 +186,8 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
                                                int ti, int tj, int nch, int64_t e, int pair,
                                                double inv2a, double *__restrict__ R,
                                                int32_t *__restrict__ status, const CUtensorMap *wmap,
-                                               const double *__restrict__ Ek, double Ee, int nlev) {
+                                               const double *__restrict__ Ek, double Ee, int nlev,
+                                               const double *__restrict__ w, int64_t ldw, int kstar) {
   double *dsm = reinterpret_cast<double *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
   uint64_t *empty = full + C::STAGES;
@@ -222,7 +223,7 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
     if (!C::PRODUCER && warp_id() == kt % C::NCW && kt + C::STAGES < nk) {
       // this warp's turn: once every warp has released slab kt, refill its slot with kt + STAGES
       mbar_wait(&empty[s], (kt / C::STAGES) & 1);
-      rform_fill<C>(smem, wmap, Ek, Ee, nlev, kt + C::STAGES, diag, ti, tj);
+      rform_fill<C>(smem, wmap, Ek, Ee, nlev, kt + C::STAGES, diag, ti, tj, kstar);
     }
   }
 
@@ -231,12 +232,15 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
   if (pole && pair == 0 && threadIdx.x == 0) set_status(status, e, RMX_E_POLE);
   double *Re = R + e * static_cast<int64_t>(nch) * nch;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  // the nearest pole's term w_ik* w_jk* d_k* / 2a, added last (reading S1)
+  const double dsc = inv2a / (__ldg(Ek + kstar) - Ee);
 #pragma unroll
   for (int u = 0; u < NBLK; ++u) {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
       const int row = ti * C::BM + rb0 * 32 + mi * 8 + prow;
       if (row >= nch) continue;
+      const double wr = __ldg(w + static_cast<int64_t>(row) * ldw + kstar);
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
 #pragma unroll
@@ -244,7 +248,8 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
           const int col = tj * C::BM + (cb0 + u) * 32 + ni * 8 + t + 4 * h;
           if (col >= nch) continue;
           if (diag && row > col) continue;  // lower half of a diagonal tile comes from its mirror
-          const double v = pole ? nan : acc[u][mi][ni][h] * inv2a;
+          const double wc = __ldg(w + static_cast<int64_t>(col) * ldw + kstar);
+          const double v = pole ? nan : fma(acc[u][mi][ni][h], inv2a, (wr * wc) * dsc);
           Re[static_cast<int64_t>(row) * nch + col] = v;
           if (row != col) Re[static_cast<int64_t>(col) * nch + row] = v;
         }
@@ -255,9 +260,10 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
 
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1)
-    rform_dmma_kernel(const __grid_constant__ CUtensorMap wmap, const double *__restrict__ Ek,
-                      const double *__restrict__ E, int nch, int nlev, int ntiles, int nen,
-                      double inv2a, double *__restrict__ R, int32_t *__restrict__ status) {
+    rform_dmma_kernel(const __grid_constant__ CUtensorMap wmap, const double *__restrict__ w, int64_t ldw,
+                      const double *__restrict__ Ek, const double *__restrict__ E, int nch, int nlev,
+                      int ntiles, int nen, double inv2a, double *__restrict__ R,
+                      int32_t *__restrict__ status) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(C::NT, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(dsm + C::STAGES * C::BK);
   uint64_t *empty = full + C::STAGES;
   int *pole_flag = reinterpret_cast<int *>(empty + C::STAGES);
+  int *kstar_s = pole_flag + 1;
 
   // energies fastest: the CTAs resident at any moment are (mostly) one tile pair for up to ~148
   // energies, so they stream the same two 128-row slabs of W in lock step and W is fetched from
@@ -284,16 +291,18 @@ __global__ void __launch_bounds__(C::NT, 1)
       mbar_init(&empty[s], C::NCW);
     }
     *pole_flag = 0;
+    *kstar_s = nearest_pole(Ek, nlev, Ee);
     fence_barrier_init();
   }
   __syncthreads();
+  const int kstar = *kstar_s;
 
   if (!C::PRODUCER) {
     // prologue: warp 0 fills the first STAGES slabs; afterwards the consumers refill in turn
     if (warp == 0) {
       tma_prefetch_desc(&wmap);
       for (int kt = 0; kt < C::STAGES && kt < nk; ++kt)
-        rform_fill<C>(smem, &wmap, Ek, Ee, nlev, kt, diag, ti, tj);
+        rform_fill<C>(smem, &wmap, Ek, Ee, nlev, kt, diag, ti, tj, kstar);
     }
   } else if (warp == C::NCW) {
     // ===================== producer warp: TMA + denominators =====================
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(C::NT, 1)
       if (k < nlev) {
         const double diff = __ldg(Ek + k) - Ee;
         if (fabs(diff) < kPoleGuard) found_pole = 1;
-        dv = 1.0 / diff;
+        dv = (k == kstar) ? 0.0 : 1.0 / diff;  // the nearest pole's term is added in the epilogue
       }
       dsm[s * C::BK + lane] = dv;
       if (found_pole) *pole_flag = 1;
@@ -336,13 +345,13 @@ __global__ void __launch_bounds__(C::NT, 1)
   const int nblk = rform_chunk<C::NB, C::NCW>(warp, rbm, cbm, diag, rb0, cb0);
   if (nblk == 2)
     rform_consumer<C, 0>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status, &wmap,
-                         Ek, Ee, nlev);
+                         Ek, Ee, nlev, w, ldw, kstar);
   else if (nblk == 1)
     rform_consumer<C, 2>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status, &wmap,
-                         Ek, Ee, nlev);
+                         Ek, Ee, nlev, w, ldw, kstar);
   else
     rform_consumer<C, 3>(smem, nk, diag, rb0, cb0, ti, tj, nch, e, pair, inv2a, R, status, &wmap,
-                         Ek, Ee, nlev);
+                         Ek, Ee, nlev, w, ldw, kstar);
 }
 
 // Small-channel path (nch <= 32, e.g. BASELINE.json:7 'tiny'): one CTA per energy, each thread owns
@@ -356,10 +365,15 @@ __global__ void __launch_bounds__(256) rform_small_kernel(const double *__restri
                                                           int32_t *__restrict__ status) {
   constexpr int PPT = 3;
   __shared__ double ds[1024];
-  __shared__ int pole;
+  __shared__ int pole, kstar_s;
   const int64_t e = blockIdx.x;
   const double Ee = E[e];
-  if (threadIdx.x == 0) pole = 0;
+  if (threadIdx.x == 0) {
+    pole = 0;
+    kstar_s = nearest_pole(Ek, nlev, Ee);
+  }
+  __syncthreads();
+  const int kstar = kstar_s;
   const int npair = nch * (nch + 1) / 2;
   int pi[PPT], pj[PPT];
   double s[PPT];
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(256) rform_small_kernel(const double *__restri
       if (k0 + k < nlev) {
         const double diff = Ek[k0 + k] - Ee;
         if (fabs(diff) < kPoleGuard) pole = 1;
-        dv = 1.0 / diff;
+        dv = (k0 + k == kstar) ? 0.0 : 1.0 / diff;  // nearest pole added last (reading S1)
       }
       ds[k] = dv;
     }
@@ -404,10 +418,11 @@ __global__ void __launch_bounds__(256) rform_small_kernel(const double *__restri
   __syncthreads();
   double *Re = R + e * static_cast<int64_t>(nch) * nch;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  const double dsc = inv2a / (Ek[kstar] - Ee);
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     if (pi[q] < 0) continue;
-    const double v = pole ? nan : s[q] * inv2a;
+    const double v = pole ? nan : fma(s[q], inv2a, (w[pi[q] * ldw + kstar] * w[pj[q] * ldw + kstar]) * dsc);
     Re[pi[q] * nch + pj[q]] = v;
     Re[pj[q] * nch + pi[q]] = v;
   }
@@ -490,7 +505,7 @@ static cudaError_t launch_rform_cfg(const double *w, int64_t ldw, const double *
   for (int64_t e0 = 0; e0 < ne; e0 += max_e) {
     const int64_t n = (ne - e0 < max_e) ? ne - e0 : max_e;
     rform_dmma_kernel<C><<<static_cast<unsigned>(n * npairs), C::NT, C::SMEM_BYTES, st>>>(
-        map, Ek, E + e0, nch, nlev, ntiles, static_cast<int>(n), inv2a,
+        map, w, ldw, Ek, E + e0, nch, nlev, ntiles, static_cast<int>(n), inv2a,
         R + e0 * static_cast<int64_t>(nch) * nch, status ? status + e0 : nullptr);
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return ce;

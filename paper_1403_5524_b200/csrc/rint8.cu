@@ -67,19 +67,29 @@ __device__ __forceinline__ int umod_small(uint32_t s, int m, float inv) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// per energy: d_k = 1/(E_k - E) into dbuf [ne][nlev], dmax [ne], pole flags (status)
+// per energy: d_k = 1/(E_k - E) into dbuf [ne][nlev] with the nearest pole's entry zeroed (its term
+// w_ik* w_jk* d_k* is added in the CRT epilogue, reading S1: the fixed-point scale of a row then
+// follows the rest of the row), its index and d in kstar / dstar [ne], dmax [ne], pole flags (status)
 __global__ void __launch_bounds__(256) oz_denom_kernel(const double *__restrict__ Ek, const double *__restrict__ E,
                                                        int nlev, double *__restrict__ dbuf,
                                                        double *__restrict__ dmax, int32_t *__restrict__ pflag,
+                                                       int32_t *__restrict__ kstar, double *__restrict__ dstar,
                                                        int32_t *__restrict__ status) {
   const int64_t e = blockIdx.x;
   const double Ee = E[e];
+  __shared__ int ks;
+  if (threadIdx.x == 0) {
+    ks = nearest_pole(Ek, nlev, Ee);
+    kstar[e] = ks;
+    dstar[e] = 1.0 / (Ek[ks] - Ee);
+  }
+  __syncthreads();
   double mx = 0.0;
   int pole = 0;
   for (int k = threadIdx.x; k < nlev; k += blockDim.x) {
     const double diff = Ek[k] - Ee;
     if (fabs(diff) < kPoleGuard) pole = 1;
-    const double d = 1.0 / diff;
+    const double d = (k == ks) ? 0.0 : 1.0 / diff;
     dbuf[e * nlev + k] = d;
     mx = fmax(mx, fabs(d));
   }
@@ -601,7 +611,10 @@ __device__ __forceinline__ double crt_value(const uint8_t *rp, int64_t plane, in
 __global__ void __launch_bounds__(256) oz_crt_tile_kernel(const uint8_t *__restrict__ res, int64_t ldr, int nch,
                                                           const int32_t *__restrict__ sx,
                                                           const int32_t *__restrict__ tw, double inv2a,
-                                                          const int32_t *__restrict__ pflag, double *__restrict__ R) {
+                                                          const int32_t *__restrict__ pflag,
+                                                          const double *__restrict__ w, int64_t ldw,
+                                                          const int32_t *__restrict__ kstar,
+                                                          const double *__restrict__ dstar, double *__restrict__ R) {
   __shared__ double tile[32][33];
   const int64_t e = blockIdx.y;
   // blockIdx.x enumerates the upper-triangle tiles (ti <= tj) row by row
@@ -618,14 +631,19 @@ __global__ void __launch_bounds__(256) oz_crt_tile_kernel(const uint8_t *__restr
   const bool pole = pflag[e] != 0;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   const int j = tj * 32 + tx;
+  // the nearest pole's term w_ik* w_jk* d_k* / 2a, added to the CRT value (reading S1)
+  const int ks = kstar[e];
+  const double dsc = dstar[e] * inv2a;
+  const double wj = j < nch ? w[static_cast<int64_t>(j) * ldw + ks] : 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int li = ty + 8 * q, i = ti * 32 + li;
     double v = 0.0;
     if (i < nch && j < nch && j >= i) {
+      const double wi = w[static_cast<int64_t>(i) * ldw + ks];
       v = pole ? nan
                : crt_value(res + e * L * plane + static_cast<int64_t>(i) * ldr + j, plane,
-                           sx[e * nch + i] + tw[j], inv2a);
+                           sx[e * nch + i] + tw[j], inv2a) + (wi * wj) * dsc;
       Re[static_cast<int64_t>(i) * nch + j] = v;
     }
     tile[li][tx] = v;
@@ -744,6 +762,7 @@ size_t rint8_ws_bytes(int64_t nch, int64_t nlev, int64_t ne) {
   b += 2 * sizeof(double) * (static_cast<size_t>(ne) * nlev + ne + static_cast<size_t>(ne) * nch);  // d, dmax, xmax
   b += sizeof(double) * nch;                                         // rowmax
   b += 2 * sizeof(int32_t) * (static_cast<size_t>(ne) * nch + ne);   // shifts, pole flags (2 buffers)
+  b += 2 * (sizeof(int32_t) + sizeof(double)) * ne + 2 * 512;        // nearest pole k*, d_k* (2 buffers)
   b += sizeof(int32_t) * nch + sizeof(int2) * 4096 + 32 * 1024;      // t_j, tile list, alignment slack
   return b;
 }
@@ -772,7 +791,8 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   int8_t *V[2];
   double *dbuf[2], *dmax[2];
   float *xmax[2];
-  int32_t *sx[2], *pflag[2];
+  int32_t *sx[2], *pflag[2], *kst[2];
+  double *dst[2];
   for (int b = 0; b < 2; ++b) {
     V[b] = reinterpret_cast<int8_t *>(carve(static_cast<size_t>(chunk) * i8::L * nch * ldv));
     dbuf[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk * nlev));
@@ -780,6 +800,8 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     dmax[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk));
     sx[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk * nch));
     pflag[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk));
+    kst[b] = reinterpret_cast<int32_t *>(carve(sizeof(int32_t) * chunk));
+    dst[b] = reinterpret_cast<double *>(carve(sizeof(double) * chunk));
   }
   uint8_t *res = carve(static_cast<size_t>(chunk) * i8::L * nch * ldr);
   double *rowmax = reinterpret_cast<double *>(carve(sizeof(double) * nch));
@@ -851,7 +873,7 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     if (c >= 2) cudaStreamWaitEvent(cs, ss.gemm_done[b], 0);  // buffer b free again
     int32_t *stc = status ? status + e0 : nullptr;
     i8::oz_denom_kernel<<<static_cast<unsigned>(n), 256, 0, cs>>>(Ek, E + e0, static_cast<int>(nlev), dbuf[b],
-                                                                      dmax[b], pflag[b], stc);
+                                                                      dmax[b], pflag[b], kst[b], dst[b], stc);
     dim3 g(static_cast<unsigned>((nlev + 2047) / 2048), static_cast<unsigned>(nch), 1);
     cudaMemsetAsync(xmax[b], 0, sizeof(float) * chunk * nch, cs);
     for (int64_t q = 0; q < n; q += 8)  // the row-maxima kernel stages at most 8 energies
@@ -887,9 +909,9 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
     gemm_mark(false);
     const int64_t ntc = (nch + 31) / 32;
     dim3 gc(static_cast<unsigned>(ntc * (ntc + 1) / 2), static_cast<unsigned>(n));
-    i8::oz_crt_tile_kernel<<<gc, 256, 0, st>>>(res, ldr, static_cast<int>(nch), sx[b], tw, inv2a, pflag[b],
-                                               R + e0 * nch * nch);
-    cudaEventRecord(ss.gemm_done[b], st);  // after the CRT: it reads sx[b] and pflag[b]
+    i8::oz_crt_tile_kernel<<<gc, 256, 0, st>>>(res, ldr, static_cast<int>(nch), sx[b], tw, inv2a, pflag[b], w,
+                                               ldw, kst[b], dst[b], R + e0 * nch * nch);
+    cudaEventRecord(ss.gemm_done[b], st);  // after the CRT: it reads sx[b], pflag[b], kst[b], dst[b]
     ce = cudaGetLastError();
     if (ce != cudaSuccess) return ce;
   }

@@ -13,6 +13,26 @@ namespace rmx {
 
 constexpr double kPoleGuard = 1e-10;  // |E - E_k| < 1e-10 Ry -> RMX_E_POLE
 
+// ---- nearest pole ----------------------------------------------------------------------------
+// Index k* of the pole nearest to E (E_k ascending, the rmx.h precondition; ties -> lower index).
+// Both R formations sum the term of k* apart from the others and add it last (reading S1):
+// next to a pole that term is orders of magnitude larger than the rest, and accumulating the rest on
+// top of it (or, for the INT8-CRT path, scaling the fixed point to it) would keep only the bits of
+// the background that survive next to the pole term.
+__device__ __forceinline__ int nearest_pole(const double *__restrict__ Ek, int nlev, double E) {
+  int lo = 0, hi = nlev;  // first k with E_k >= E
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (Ek[mid] < E)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  if (lo >= nlev) return nlev - 1;
+  if (lo == 0) return 0;
+  return (E - Ek[lo - 1] <= Ek[lo] - E) ? lo - 1 : lo;
+}
+
 // ---- status helpers (first error wins) ---------------------------------------------------
 __device__ __forceinline__ void set_status(int32_t *status, int64_t e, int32_t code) {
   if (status != nullptr && code != 0) atomicCAS(reinterpret_cast<int *>(status + e), 0, code);

@@ -13,10 +13,11 @@
 // two real planes (re, im) and every complex product is two real DMMA GEMMs whose k range covers
 // both halves (GemmArgs::nseg = 2):
 //   0. Ar = I, Ai = -K_oo
-//   1. blocked right-looking LDL^T, blocks of 64: the diagonal block is factored in shared memory
-//      together with the inverse of its unit-lower factor, Tinv_b = L_bb^{-1} (written over the
-//      block, D to a vector); W21 = A21 Tinv_b^T (= L21 D_b), L21 = W21 D_b^{-1}, and the trailing
-//      update A22 -= W21 L21^T (lower tiles)
+//   1. blocked right-looking LDL^T, outer blocks of 128 made of two 64-wide sub-blocks: each 64 x 64
+//      diagonal block is factored in shared memory together with the inverse of its unit-lower
+//      factor, Tinv_b = L_bb^{-1} (written over the block, D to a vector); W21 = A21 Tinv_b^T
+//      (= L21 D_b), L21 = W21 D_b^{-1}; the second sub-block's columns are updated inside the panel,
+//      and the trailing matrix once per 128 columns, A22 -= W21 L21^T (lower tiles, K = 128)
 //   2. Z = L^{-1} in place, 128-row block rows: the 128 x 128 diagonal inverse from the two 64
 //      inverses, Z_{B,0:B} = -Tinv_B (L_{B,0:B} Z_{0:B,0:B})
 //   3. Y = D^{-1} Z
@@ -154,6 +155,28 @@ __device__ __noinline__ void diag_ldlt_inv(const MatView &ar, const MatView &ai,
   __syncthreads();
 }
 
+// L = W D^{-1}: dst[(dr0 + i, dc0 + j)] = src[(sr0 + i, sc0 + j)] / d_j (complex), i < m, j < w <= 64.
+__device__ __forceinline__ void scale_cols(const MatView &sr, const MatView &si, int sr0, int sc0,
+                                           const MatView &tr, const MatView &ti, int dr0, int dc0, int m, int w,
+                                           const double *dre, const double *dim, double *sm) {
+  double *idr = sm, *idi = sm + 64;
+  __syncthreads();
+  for (int j = threadIdx.x; j < w; j += NT) {
+    const double a = dre[j], b = dim[j], den = fma(a, a, b * b);
+    idr[j] = a / den;
+    idi[j] = -b / den;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < m * 64; q += NT) {
+    const int i = q >> 6, j = q & 63;
+    if (j < w) {
+      const double xr = *sr.at(sr0 + i, sc0 + j), xi = *si.at(sr0 + i, sc0 + j);
+      *tr.at(dr0 + i, dc0 + j) = xr * idr[j] - xi * idi[j];
+      *ti.at(dr0 + i, dc0 + j) = fma(xr, idi[j], xi * idr[j]);
+    }
+  }
+}
+
 // Complex product into the planes (cr, ci) at (r0, c0): C = alpha * (A.B) (set) or C -= A.B (sub),
 // A = (a_re, a_im), B = (b_re, b_im) given as operand pairs of one layout.
 __device__ __forceinline__ void cgemm(int M, int N, int K, const Op &are, const Op &aim, const Op &bre,
@@ -247,37 +270,41 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       TPH_MARK(0);  // copy (+ photo v)
-      // 1. blocked LDL^T
-      for (int P0 = 0; P0 < o; P0 += CB) {
-        const int W = min(CB, o - P0), m = o - P0 - W;
-        diag_ldlt_inv(Arv, Aiv, P0, W, dr, di, sm.tri);
+      // 1. blocked LDL^T, outer blocks of 128 = two 64-wide sub-blocks (diagonal factor + inverse in
+      // shared memory each); the trailing update runs once per 128 columns (K = 2 x 128 per C pass)
+      for (int P0 = 0; P0 < o; P0 += 2 * CB) {
+        const int W = min(2 * CB, o - P0), W1 = min(CB, W), W2 = W - W1, mb = o - P0 - W1, m = o - P0 - W;
+        // Y scratch row q <-> global row P0 + W1 + q; columns [0, W1) sub-block 1, [W1, W) sub-block 2
+        diag_ldlt_inv(Arv, Aiv, P0, W1, dr, di, sm.tri);
         TPH_MARK(1);  // diagonal blocks
-        if (m > 0) {
-          // W21 = A21 Tinv^T -> Y planes [0, m) x [0, W)
-          cgemm(m, W, W, opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0), opk(Arv, P0, P0), opk(Aiv, P0, P0),
+        if (mb > 0) {
+          // W21 = A21 T1^T (= L21 D1) for all rows below sub-block 1
+          cgemm(mb, W1, W1, opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0), opk(Arv, P0, P0), opk(Aiv, P0, P0),
                 Yrv, Yiv, 0, 0, false, false, 1.0, 0, smg, gs);
           TPH_MARK(2);  // W21 = A21 Tinv^T
-          // L21 = W21 D^{-1} over A21
-          double *idr = sm.tri, *idi = sm.tri + CB;
-          for (int j = threadIdx.x; j < W; j += NT) {
-            const double a = dr[P0 + j], b = di[P0 + j], den = fma(a, a, b * b);
-            idr[j] = a / den;
-            idi[j] = -b / den;
-          }
-          __syncthreads();
-          for (int q = threadIdx.x; q < m * CB; q += NT) {
-            const int i = q / CB, j = q % CB;
-            if (j < W) {
-              const double xr = *Yrv.at(i, j), xi = *Yiv.at(i, j);
-              *Arv.at(P0 + W + i, P0 + j) = xr * idr[j] - xi * idi[j];
-              *Aiv.at(P0 + W + i, P0 + j) = fma(xr, idi[j], xi * idr[j]);
+          scale_cols(Yrv, Yiv, 0, 0, Arv, Aiv, P0 + W1, P0, mb, W1, dr + P0, di + P0, sm.tri);
+          TPH_MARK(3);  // L21 scaling
+          if (W2 > 0) {
+            // sub-block 2's columns: A[P0+W1:, P0+W1:P0+W] -= W21 L21[0:W2]^T
+            cgemm(mb, W2, W1, opk(Yrv, 0, 0), opk(Yiv, 0, 0), opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0),
+                  Arv, Aiv, P0 + W1, P0 + W1, false, true, 1.0, 0, smg, gs);
+            TPH_MARK(4);
+            diag_ldlt_inv(Arv, Aiv, P0 + W1, W2, dr, di, sm.tri);
+            TPH_MARK(1);
+            if (m > 0) {
+              cgemm(m, W2, W2, opk(Arv, P0 + W, P0 + W1), opk(Aiv, P0 + W, P0 + W1), opk(Arv, P0 + W1, P0 + W1),
+                    opk(Aiv, P0 + W1, P0 + W1), Yrv, Yiv, W2, W1, false, false, 1.0, 0, smg, gs);
+              TPH_MARK(2);
+              scale_cols(Yrv, Yiv, W2, W1, Arv, Aiv, P0 + W, P0 + W1, m, W2, dr + P0 + W1, di + P0 + W1, sm.tri);
+              TPH_MARK(3);
             }
           }
-          TPH_MARK(3);  // L21 scaling
-          // A22 -= W21 L21^T (lower tiles)
-          cgemm(m, m, W, opk(Yrv, 0, 0), opk(Yiv, 0, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0),
-                Arv, Aiv, P0 + W, P0 + W, true, true, 1.0, 0, smg, gs);
-          TPH_MARK(4);  // trailing updates
+          if (m > 0) {
+            // A22 -= [W21 W22] [L21 L22]^T (lower tiles), K = W per product
+            cgemm(m, m, W, opk(Yrv, W2, 0), opk(Yiv, W2, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0),
+                  Arv, Aiv, P0 + W, P0 + W, true, true, 1.0, 0, smg, gs);
+            TPH_MARK(4);  // trailing updates
+          }
         }
       }
       // 2. Z = L^{-1} in place, 128-row block rows

@@ -88,3 +88,52 @@ def test_block_cyclic_balances_darc_cost():
     assert contiguous > 0.15                               # measured 0.186
     assert rdist.imbalance(cost, 16, 8) < 2e-3             # fine blocks: ~1e-3
     assert rdist.imbalance(cost, 296, 8) < 0.03            # bench batch (2 x 148): 0.0185
+
+
+def _worker_case(rank, world, port, out_q):
+    """bench.py's N > 1 input path: rank 0 generates the case, the other ranks generate nothing and
+    receive W, E_k, thresholds and mesh (rdist.broadcast_case); then a bench-style gather of the
+    row sums of the blocks each rank processed (explicit shards), reassembled in mesh order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    rdist.init_process_group("gloo")
+    try:
+        case = syn.make_case("tiny") if rank == 0 else None
+        w, Ek, eps, E, a = rdist.broadcast_case(case, torch.device("cpu"))
+        ne, block, steps = len(E), 64, 3
+        shards = []
+        for r in range(world):  # bench.py timed_shards: `steps` blocks spread over the rank's blocks
+            blocks = rdist.cyclic_blocks(ne, block, world, r)
+            shards.append(np.concatenate([np.arange(*rdist.block_range(blocks[int((s + 0.5) * len(blocks) / steps)],
+                                                                         ne, block)) for s in range(steps)]))
+        mine = torch.from_numpy(np.stack([E.numpy()[shards[rank]], -E.numpy()[shards[rank]]], axis=1))
+        full = rdist.gather_summaries(mine, ne, block, world, shards)
+        out_q.put((rank, w.numpy().copy(), Ek.numpy().copy(), eps.numpy().copy(), E.numpy().copy(), a,
+                   full.numpy().copy(), [s.tolist() for s in shards]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_broadcast_case_and_partial_gather():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_case, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c = syn.make_case("tiny")
+    for rank, w, Ek, eps, E, a, full, shards in res:
+        assert w.shape == (c.nch, c.nlev + (c.nlev & 1))
+        assert np.array_equal(w[:, :c.nlev], c.w) and np.all(w[:, c.nlev:] == 0)
+        assert np.array_equal(Ek, c.Ek) and np.array_equal(eps, c.eps) and np.array_equal(E, c.E)
+        assert a == c.a
+        covered = np.concatenate([np.array(s) for s in shards])
+        assert len(np.unique(covered)) == len(covered)
+        expect = np.zeros((len(E), 2))
+        expect[covered, 0], expect[covered, 1] = E[covered], -E[covered]
+        assert np.array_equal(full, expect), rank
