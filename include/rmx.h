@@ -74,8 +74,10 @@ const char *rmx_last_error(const rmx_ctx *ctx);
 /*
  * rmx_build_R - S1+S2: R_ij(E_e) = (1/2a) sum_k w_ik w_jk / (E_k - E_e)   (Eq.1-2;
  * BASELINE.json:5). Upper triangle computed by an energy-batched FP64 DMMA contraction with
- * TMA-staged W tiles; the denominators 1/(E_k - E) are formed on chip, never stored. R is
- * written full and BITWISE symmetric (upper triangle mirrored).
+ * TMA-staged W tiles (or, after rmx_set_r_algo(RMX_R_INT8), exactly on the INT8 tensor cores);
+ * the denominators 1/(E_k - E) are formed on chip, never stored. The term of the pole nearest to
+ * E_e is summed apart and added last (reading N1: keeps the rest of the sum accurate next
+ * to a pole). R is written full and BITWISE symmetric (upper triangle mirrored).
  *   w      DEVICE [nch][ldw]  amplitudes, k contiguous; ldw >= nlev, ldw even (ldw*8 % 16 == 0,
  *                             TMA stride rule) and w 16-byte aligned
  *   Ek     DEVICE [nlev]      poles, ascending
@@ -106,9 +108,10 @@ rmx_rc rmx_match_K(rmx_ctx *ctx, const double *R, const double *F, const double 
                    const int32_t *n_open, double *K, int32_t *status);
 
 /*
- * rmx_collision_strength - S5: T = 2i K_oo (I - i K_oo)^{-1}, o = n_open, via the real
- * SPD route (BASELINE.json:5; reading T2): S = I + K_oo K_oo^T, Cholesky S = LL^T,
- * X = S^{-1} K_oo, P = K_oo X; then Re T = -2P, Im T = 2X and |T_ij|^2 = 4(X_ij^2 + P_ij^2).
+ * rmx_collision_strength - S5: T = 2i K_oo (I - i K_oo)^{-1}, o = n_open (BASELINE.json:5;
+ * DESIGN.md reading T2): with A = I - i K_oo, T = 2(A^{-1} - I); A^{-1} from a complex-symmetric
+ * LDL^T without pivoting (A's Hermitian part is I, so every pivot has Re d >= 1) per energy, FP64
+ * DMMA GEMMs; |T_ij|^2 = 4 |(A^{-1})_ij - delta_ij|^2 (error ~u ||K_oo||, bitwise symmetric).
  *   K       DEVICE [ne][nch][nch] (only the open block is read)
  *   T2      DEVICE [ne][nch][nch] or NULL: |T|^2, open block top-left, 0 elsewhere
  *   rowsum  DEVICE [ne][nch] or NULL: sum_j |T_ij|^2 (0 for closed rows)
@@ -210,8 +213,8 @@ rmx_rc rmx_dipole_amplitude(rmx_ctx *ctx, const double *w, int64_t ldw, const do
 
 /*
  * rmx_photoionization - steps (10)-(12) from K (rmx_match_K output, all rows, closed columns -e_j)
- * and g: v, then M by the real SPD route y = (I + K_oo^2)^{-1} v, M = y + i K_oo y (K_oo symmetric,
- * reading M1), per-channel |M_j|^2 and sigma.
+ * and g: v, then M = (I - i K_oo)^{-1} v with the inverse of the T route (rmx_collision_strength),
+ * per-channel |M_j|^2 and sigma.
  *   K DEVICE [ne][nch][nch]; g, Fp, Gp DEVICE [ne][nch]; E DEVICE [ne]; n_open DEVICE int32 [ne] or NULL
  *   E0     initial (bound) state energy: photon energy = E - E0
  *   C      cross-section prefactor (e.g. 4 pi^2 alpha / 3 = 0.0960769... in atomic units)
@@ -225,7 +228,7 @@ rmx_rc rmx_photoionization(rmx_ctx *ctx, const double *K, const double *g, const
 
 /*
  * rmx_sweep_photo - the fused photoionisation sweep: per batch R -> K (as rmx_sweep), g, then the
- * T-route Cholesky with v as one extra right-hand side; only sigma [ne] (and optionally
+ * T-route inverse applied to v; only sigma [ne] (and optionally
  * mabs2 [ne][nch]) and status leave the device. Arguments as rmx_sweep plus d, E0, C.
  */
 rmx_rc rmx_sweep_photo(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek, const double *d,

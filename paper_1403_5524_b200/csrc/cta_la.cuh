@@ -1,5 +1,5 @@
 // cta_la.cuh - CTA-level dense FP64 linear algebra on one matrix in global memory, used by the
-// per-energy matching (LU) and T-epilogue (Cholesky) kernels. Every routine is executed by all NT
+// per-energy matching (LU) and T-epilogue (complex LDL^T, tepi.cu) kernels. Every routine is executed by all NT
 // threads of one CTA; there is no inter-CTA communication (one CTA owns one energy, SURVEY.md
 // §8(a) S4/S5 and BASELINE.json:5 "one CTA ... per energy").
 //
@@ -8,9 +8,9 @@
 //               B stored [N][K] or [K][N]; C read (C -= A.B) or written (C = A.B)
 //   panel_lu  : unblocked LU with partial pivoting of an n x bw panel (pivot = max |a|, ties ->
 //               lowest row, the oracle's rule), rank-1 updates fused with the next pivot search
-//   tri_inv   : inverse of a 32 x 32 triangular diagonal block; all triangular solves are then
-//               DMMA GEMMs with it (in place)
-//   chol_diag : unblocked Cholesky of a bw x bw diagonal block in shared memory
+//   tri_inv128: inverse of a 128 x 128 triangular diagonal block (64 x 64 halves by substitution in
+//               shared memory, the off-diagonal block by two DMMA GEMMs); the triangular solves
+//               of the LU are then DMMA GEMMs with it (MAGMA-style inverted diagonal blocks)
 #pragma once
 #include "rmx_common.cuh"
 
@@ -37,12 +37,10 @@ constexpr int CS_LD = BN + 2;  // C tile pitch (bulk row copies): 4 rows = 64 mo
 constexpr int C_ELEMS = BM * CS_LD;
 constexpr int GEMM_SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_ELEMS * 8;  // + 1024 alignment slack
 constexpr int GEMM_SMEM_DOUBLES = GEMM_SMEM_BYTES / 8;
-constexpr int TRI_LD = PB + 1;                // padded pitch of a bw x bw triangle in smem
 constexpr int TB = 64;                        // edge of the smem-computed triangular inverses
 constexpr int TB_LD = TB + 1;
 constexpr int TG = NB;                        // edge (and pitch) of the global inverse Tg (128)
-constexpr int CH_LD = NB + 1;                 // pitch of the smem Cholesky block
-constexpr int TRI_SMEM_DOUBLES = (2 * TB * TB_LD > NB * CH_LD) ? 2 * TB * TB_LD : NB * CH_LD;
+constexpr int TRI_SMEM_DOUBLES = 2 * TB * TB_LD;  // tri_inv64 scratch
 
 // A matrix of a workspace slot: raw pointer + leading dimension, and its TMA descriptors
 // (NVIEW box shapes, see above; the tensor extent is the matrix allocation, out-of-range
@@ -286,6 +284,10 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
+      // lower mode: a warp tile entirely above the diagonal (its last row < its first column) only
+      // keeps the ring protocol (waits and arrivals): no DMMA, no store - the callers never read
+      // the strict upper part of a lower-tile result (DMMA pipe time on the diagonal tiles)
+      const bool upper_only = lower && (tm * BM + wm * WTM + WTM - 1 < tn * BN + wn * WTN);
       for (int sg = 0; sg < ga.nseg; ++sg) {
       // sign of the second product: flip the sign bit of its A fragments (integer op, off the
       // FP64 pipe)
@@ -293,6 +295,11 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
       for (int kc = kc_first(ga.kband, tm, tn); kc < nkc; ++kc, ++it) {
         const int st = it % STAGES, use = it / STAGES;
         mbar_wait(&gs->full[st], use & 1);
+        if (upper_only) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&gs->empty[st]);
+          continue;
+        }
         const int krem = min(BK, K - kc * BK);
         const uint32_t sa = smem0 + st * STAGE_BYTES, sb = sa + A_STAGE_BYTES;
         auto step = [&](const int k8, const bool partial) {
@@ -354,7 +361,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
       }
       // epilogue: this warp's 32 x 32 part of the tile straight to global memory
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) {
+      for (int mi = 0; mi < (upper_only ? 0 : MI); ++mi) {
         const int r = tm * BM + wm * WTM + mi * 8 + arow;
         if (r >= M) continue;
         double *crow = ga.C + static_cast<int64_t>(r) * ga.ldc;
@@ -404,13 +411,6 @@ __device__ __forceinline__ void gemm_sub(int M, int N, int K, const Op &a, const
   GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, true, false, 0.0};
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
-// C = A.B with a known-zero leading k band (GemmArgs::kband)
-__device__ __forceinline__ void gemm_set_kb(int M, int N, int K, const Op &a, const Op &b,
-                                            const MatView &c, int cr0, int cc0, bool lower, int kband,
-                                            double *smem, GemmSync *gs) {
-  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, false, 0.0, kband};
-  gemm_rt(ga, gemm_smem_align(smem), gs);
-}
 // C = A.B + diag_add I
 __device__ __forceinline__ void gemm_set(int M, int N, int K, const Op &a, const Op &b,
                                          const MatView &c, int cr0, int cc0, bool lower,
@@ -418,18 +418,6 @@ __device__ __forceinline__ void gemm_set(int M, int N, int K, const Op &a, const
   GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, false, diag_add};
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
-// C^T = A.B: element (i, j) of the product goes to the submatrix of `c` at (r0 + j, c0 + i).
-// In-place use is safe when the operand being overwritten is B and M <= BM (one tile row): each
-// output tile then depends only on its own rows of B.
-// NOTE: any in-place GEMM must have its overwritten operand confined to one tile row / column;
-// otherwise a later tile would read values an earlier tile already stored.
-__device__ __forceinline__ void gemm_set_t(int M, int N, int K, const Op &a, const Op &b,
-                                           const MatView &c, int cr0, int cc0, double *smem,
-                                           GemmSync *gs) {
-  GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, false, false, true, 0.0};
-  gemm_rt(ga, gemm_smem_align(smem), gs);
-}
-
 // ------------------------------------------------------------------------------------------------
 // Block-wide argmax of |value| with ties -> lowest index. red: smem [2*NW] scratch.
 __device__ __forceinline__ void block_argmax(double &v, int &idx, double *redv, int *redi) {
@@ -600,104 +588,7 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
   return singular;
 }
 
-// Inverse of a bw x bw (bw <= PB) triangular diagonal block src[p0.., p0..] written to the global
-// scratch Tg [PB][PB] (zero padded), so that every triangular solve of the factorizations becomes a
-// DMMA GEMM with this inverse (MAGMA-style inverted diagonal blocks).
-//   kind 0: unit lower (strict lower part of src)   kind 1: lower (non-unit)   kind 2: upper (non-unit)
-// All threads stage the block into smem; warp 0 computes column c of the inverse in lane c by
-// substitution (registers, fixed-size unrolled loops); all threads then write Tg.
 enum { TRI_UNIT_LOWER = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
-__device__ __forceinline__ void tri_inv(const double *src, int64_t ld, int p0, int bw, int kind,
-                                        double *tri, double *Tg) {
-  __syncthreads();
-  for (int q = threadIdx.x; q < PB * PB; q += NT) {
-    const int r = q / PB, c = q % PB;
-    double v = 0.0;
-    if (r < bw && c < bw) {
-      const bool keep = kind == TRI_UPPER ? (c >= r) : (kind == TRI_LOWER ? (c <= r) : (c < r));
-      if (keep) v = src[static_cast<int64_t>(p0 + r) * ld + p0 + c];
-    }
-    if (kind == TRI_UNIT_LOWER && r == c) v = 1.0;
-    if (r >= bw && r == c) v = 1.0;  // identity padding keeps the unrolled substitution finite
-    tri[r * TRI_LD + c] = v;
-  }
-  __syncthreads();
-  if (warp_id() == 0) {
-    const int c = lane_id();
-    double x[PB];
-    if (kind != TRI_UPPER) {
-#pragma unroll
-      for (int r = 0; r < PB; ++r) {
-        double s = (r == c) ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = 0; q < r; ++q) s = fma(-tri[r * TRI_LD + q], x[q], s);
-        x[r] = (kind == TRI_LOWER) ? s / tri[r * TRI_LD + r] : s;
-      }
-    } else {
-#pragma unroll
-      for (int r = PB - 1; r >= 0; --r) {
-        double s = (r == c) ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = r + 1; q < PB; ++q) s = fma(-tri[r * TRI_LD + q], x[q], s);
-        x[r] = s / tri[r * TRI_LD + r];
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < PB; ++r) tri[r * TRI_LD + c] = (r < bw && c < bw) ? x[r] : 0.0;
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < PB * PB; q += NT) Tg[q] = tri[(q / PB) * TRI_LD + (q % PB)];
-  __syncthreads();
-}
-
-// Lower triangle L = S[p0:p0+bw, p0:p0+bw] -> tri (full bw x bw, upper part zero).
-__device__ __forceinline__ void load_lower_tri(const double *S, int64_t ld, int p0, int bw,
-                                               double *tri) {
-  for (int q = threadIdx.x; q < bw * bw; q += NT) {
-    const int r = q / bw, c = q % bw;
-    tri[r * TRI_LD + c] = c <= r ? S[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
-  }
-  __syncthreads();
-}
-
-// Unblocked Cholesky of S[p0:p0+bw, p0:p0+bw] (lower) in tri, written back to S.
-// Returns 1 if a non-positive pivot appears (S is SPD by construction: I + K K^T).
-__device__ __forceinline__ int chol_diag(double *S, int64_t ld, int p0, int bw, double *tri) {
-  load_lower_tri(S, ld, p0, bw, tri);
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  if (warp_id() == 0) {
-    const int lane = lane_id();
-    for (int c = 0; c < bw; ++c) {
-      // lane r (r >= c) holds column c of row r
-      double d = tri[c * TRI_LD + c];
-      if (lane == 0 && !(d > 0.0)) bad = 1;
-      d = sqrt(d);
-      __syncwarp();
-      if (lane >= c && lane < bw) {
-        const double v = (lane == c) ? d : tri[lane * TRI_LD + c] / d;
-        tri[lane * TRI_LD + c] = v;
-      }
-      __syncwarp();
-      if (lane > c && lane < bw) {
-        const double lr = tri[lane * TRI_LD + c];
-        for (int q = c + 1; q <= lane; ++q) tri[lane * TRI_LD + q] = fma(-lr, tri[q * TRI_LD + c], tri[lane * TRI_LD + q]);
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < bw * bw; q += NT) {
-    const int r = q / bw, c = q % bw;
-    if (c <= r) S[static_cast<int64_t>(p0 + r) * ld + p0 + c] = tri[r * TRI_LD + c];
-  }
-  __syncthreads();
-  return bad;
-}
-
-
 // Inverse of the W x W (W <= 64) diagonal block of `src` at (p0, p0) written to Tg [64][64]
 // (global, zero outside W x W): two 32 x 32 diagonal inverses by substitution (warps 0 and 1,
 // lane = column), then the off-diagonal block from the 2 x 2 block formula
@@ -783,44 +674,6 @@ __device__ __forceinline__ void tri_inv64(const double *src, int64_t ld, int p0,
   }
   __syncthreads();
 }
-
-// Unblocked Cholesky of the W x W (W <= NB) diagonal block S[p0.., p0..] (lower) in shared
-// memory, written back to S. Returns 1 if a non-positive pivot appears (S = I + K K^T is SPD).
-__device__ __forceinline__ int chol_diag_blk(double *S, int64_t ld, int p0, int W, double *sm) {
-  double *Lb = sm;
-  __shared__ int bad64;
-  __syncthreads();
-  if (threadIdx.x == 0) bad64 = 0;
-  for (int q = threadIdx.x; q < W * W; q += NT) {
-    const int r = q / W, c = q % W;
-    Lb[r * CH_LD + c] = c <= r ? S[static_cast<int64_t>(p0 + r) * ld + p0 + c] : 0.0;
-  }
-  __syncthreads();
-  for (int c = 0; c < W; ++c) {
-    const double d2 = Lb[c * CH_LD + c];
-    const double d = sqrt(d2);
-    __syncthreads();  // everyone has read the pivot before it is overwritten
-    if (threadIdx.x == 0) {
-      if (!(d2 > 0.0)) bad64 = 1;
-      Lb[c * CH_LD + c] = d;
-    }
-    for (int r = c + 1 + threadIdx.x; r < W; r += NT) Lb[r * CH_LD + c] /= d;
-    __syncthreads();
-    const int m = W - c - 1;  // trailing block rows/cols c+1..W-1, lower part
-    for (int q = threadIdx.x; q < m * m; q += NT) {
-      const int r = c + 1 + q / m, k = c + 1 + q % m;
-      if (k <= r) Lb[r * CH_LD + k] = fma(-Lb[r * CH_LD + c], Lb[k * CH_LD + c], Lb[r * CH_LD + k]);
-    }
-    __syncthreads();
-  }
-  for (int q = threadIdx.x; q < W * W; q += NT) {
-    const int r = q / W, c = q % W;
-    if (c <= r) S[static_cast<int64_t>(p0 + r) * ld + p0 + c] = Lb[r * CH_LD + c];
-  }
-  __syncthreads();
-  return bad64;
-}
-
 
 // Inverse of the W x W (W <= NB = 128) triangular diagonal block of `sv` at (p0, p0) into the
 // global Tg [128][128] (view tv, zero outside W x W): 64 x 64 diagonal inverses in shared memory

@@ -11,8 +11,8 @@
 // status RMX_E_POLE and NaN amplitudes. 2 nch nlev flops per energy - 1/(nch+1) of R formation, so
 // the kernel is a small fraction of the sweep; its bound is FP64 FMA issue.
 //
-// Steps (10)-(12) (v = (1/2) U'^T g, M = (I - iK_oo)^{-1} v via the SPD route, sigma) run inside the
-// T epilogue (tepi.cu), which already holds the Cholesky factor of I + K_oo^2.
+// Steps (10)-(12) (v = (1/2) U'^T g, M = (I - iK_oo)^{-1} v, sigma) run inside the T epilogue
+// (tepi.cu), which already holds (I - iK_oo)^{-1}.
 #include "rmx_common.cuh"
 #include "rmx_internal.h"
 #include <algorithm>

@@ -1,9 +1,11 @@
 // rform.cu - S1+S2 of the sweep: R_ij(E) = (1/2a) sum_k w_ik w_jk / (E_k - E)
 // (§6 Eq. 1-2 "R = X x Y" with X_ik = w_ik/(E - E_k), Y = w_kj; written in the
 // north_star convention of BASELINE.json:5). B200 design:
-//   * one CTA per (energy, upper-triangle tile pair (I <= J)); grid enumerates tile pairs fastest so
-//     the CTAs resident at any time stream the same W k-slabs through L2 (W read from HBM ~once per
-//     energy wave instead of once per tile pair);
+//   * one CTA per (energy, upper-triangle tile pair (I <= J)); the grid enumerates energies fastest,
+//     so the CTAs resident at any time are (mostly) one tile pair for ~148 energies and stream the
+//     same two W slabs through L2 in lock step (W read from HBM about once per wave);
+//   * the term of the pole nearest to E is left out of the k loop (d_k* = 0) and added in the
+//     epilogue (reading N1);
 //   * a producer warp issues 2D TMA loads (SWIZZLE_128B, 16 doubles x BM rows per box) of the W rows of
 //     tile I and tile J into a STAGES-deep mbarrier ring, and computes the stage's denominators
 //     d_k = 1/(E_k - E) on chip (X of Eq. 2 is never materialised) plus the pole guard;
@@ -232,7 +234,7 @@ __device__ __forceinline__ void rform_consumer(uint8_t *smem, int nk, bool diag,
   if (pole && pair == 0 && threadIdx.x == 0) set_status(status, e, RMX_E_POLE);
   double *Re = R + e * static_cast<int64_t>(nch) * nch;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  // the nearest pole's term w_ik* w_jk* d_k* / 2a, added last (reading S1)
+  // the nearest pole's term w_ik* w_jk* d_k* / 2a, added last (reading N1)
   const double dsc = inv2a / (__ldg(Ek + kstar) - Ee);
 #pragma unroll
   for (int u = 0; u < NBLK; ++u) {
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(256) rform_small_kernel(const double *__restri
       if (k0 + k < nlev) {
         const double diff = Ek[k0 + k] - Ee;
         if (fabs(diff) < kPoleGuard) pole = 1;
-        dv = (k0 + k == kstar) ? 0.0 : 1.0 / diff;  // nearest pole added last (reading S1)
+        dv = (k0 + k == kstar) ? 0.0 : 1.0 / diff;  // nearest pole added last (reading N1)
       }
       ds[k] = dv;
     }

@@ -68,7 +68,7 @@ __device__ __forceinline__ int umod_small(uint32_t s, int m, float inv) {
 
 // ---------------------------------------------------------------------------------------------
 // per energy: d_k = 1/(E_k - E) into dbuf [ne][nlev] with the nearest pole's entry zeroed (its term
-// w_ik* w_jk* d_k* is added in the CRT epilogue, reading S1: the fixed-point scale of a row then
+// w_ik* w_jk* d_k* is added in the CRT epilogue, reading N1: the fixed-point scale of a row then
 // follows the rest of the row), its index and d in kstar / dstar [ne], dmax [ne], pole flags (status)
 __global__ void __launch_bounds__(256) oz_denom_kernel(const double *__restrict__ Ek, const double *__restrict__ E,
                                                        int nlev, double *__restrict__ dbuf,
@@ -561,9 +561,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
 
 // ---------------------------------------------------------------------------------------------
 // CRT: residues r_l of P_ij -> P_ij -> R_ij. Direct formula: with C_l = (M/m_l)((M/m_l)^-1 mod m_l),
-// S = sum_l r_l C_l = P (mod M), and S/M = sum_l r_l f_l with f_l = C_l/M = inv_l/m_l in (0, 1); since
-// |P| < 2^121.3 < M/16, q = rint(sum_l r_l f_l) (fp64 error < 1e-11) is exactly the multiple of M to
-// remove, and P = S - q M is evaluated exactly in 128-bit wrapping arithmetic (4 x 32-bit limbs).
+// S = sum_l r_l C_l = P (mod M), and S/M = sum_l r_l f_l with f_l = C_l/M = inv_l/m_l in (0, 1), so
+// S/M = P/M + an integer. |P| <= nlev 2^54 2^52 = nlev 2^106 < M/2 (M = 2^125.19: |P|/M <= 0.07 at
+// nlev 40000 and 0.23 at the supported maximum nlev 131071), and the fp64 sum of the 16 terms (< 4096)
+// errs by < 1e-11, so q = rint(sum_l r_l f_l) is exactly the multiple of M to remove; P = S - q M is
+// then evaluated exactly in 128-bit wrapping arithmetic (4 x 32-bit limbs).
 struct CrtConst {
   uint32_t C[L][4];  // C_l, little-endian limbs
   double f[L];       // inv_l / m_l
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(256) oz_crt_tile_kernel(const uint8_t *__restr
   const bool pole = pflag[e] != 0;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   const int j = tj * 32 + tx;
-  // the nearest pole's term w_ik* w_jk* d_k* / 2a, added to the CRT value (reading S1)
+  // the nearest pole's term w_ik* w_jk* d_k* / 2a, added to the CRT value (reading N1)
   const int ks = kstar[e];
   const double dsc = dstar[e] * inv2a;
   const double wj = j < nch ? w[static_cast<int64_t>(j) * ldw + ks] : 0.0;
@@ -748,6 +750,8 @@ int64_t rint8_chunk(int64_t nch, int64_t nlev, int64_t ne, int nsm) {
   int64_t chunk = std::max<int64_t>(8, std::min<int64_t>(64, (want + 7) / 8 * 8));
   const int64_t per_energy = 2 * 16 * nch * rint8_ldv(nlev);
   while (chunk > 8 && chunk * per_energy > (static_cast<int64_t>(24) << 30)) chunk -= 8;
+  // very large nch x nlev: fewer than 8 energies per chunk (down to 1) rather than no INT8 path
+  while (chunk > 1 && chunk * per_energy > (static_cast<int64_t>(24) << 30)) chunk /= 2;
   return std::min(chunk, ne);
 }
 

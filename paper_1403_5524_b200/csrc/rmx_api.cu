@@ -66,6 +66,7 @@ struct rmx_ctx {
   Dev dg, dgpart;
   // R-formation algorithm (RMX_R_DMMA / RMX_R_INT8) and the INT8-CRT workspace
   int r_algo = RMX_R_DMMA;
+  int64_t r_fallbacks = 0;  // INT8-CRT requests served by the DMMA kernel (workspace did not fit)
   Dev dz;
   Int8Streams i8s;
   // instrumentation
@@ -281,8 +282,12 @@ static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double
     const int64_t chunk = rint8_chunk(nch, nlev, ne, c->nsm);
     const size_t need = rint8_ws_bytes(nch, nlev, chunk);
     if (grow(c, c->dz, need) != RMX_OK) {
-      err = "INT8-CRT workspace allocation failed";
-      return cudaErrorMemoryAllocation;
+      // not enough device memory for the INT8-CRT workspace: the FP64 DMMA formation computes the
+      // same R (counted in rmx_stats as an RMX_KID_RFORM launch like the INT8 path)
+      c->err.clear();
+      c->r_fallbacks += 1;
+      *nl = 1;
+      return launch_rform(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->stream, err);
     }
     if (!c->i8s.aux) {
       cudaStreamCreateWithFlags(&c->i8s.aux, cudaStreamNonBlocking);

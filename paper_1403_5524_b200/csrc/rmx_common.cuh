@@ -15,7 +15,7 @@ constexpr double kPoleGuard = 1e-10;  // |E - E_k| < 1e-10 Ry 
 
 // ---- nearest pole ----------------------------------------------------------------------------
 // Index k* of the pole nearest to E (E_k ascending, the rmx.h precondition; ties -> lower index).
-// Both R formations sum the term of k* apart from the others and add it last (reading S1):
+// Both R formations sum the term of k* apart from the others and add it last (reading N1):
 // next to a pole that term is orders of magnitude larger than the rest, and accumulating the rest on
 // top of it (or, for the INT8-CRT path, scaling the fixed point to it) would keep only the bits of
 // the background that survive next to the pole term.

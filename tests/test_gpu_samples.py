@@ -6,12 +6,13 @@ rmx_sweep in both R formations - the bench default (exact INT8-CRT on tcgen05) a
 kernel - and stage by stage (GPU K from the oracle's R, GPU |T|^2 from the oracle's K).
 
 Bars (BASELINE.json:5, normwise per energy, reading T1): R 1e-10, K_oo 1e-10, |T|^2 and row sums
-1e-8. The only exclusion is reading T4's fp64 floor for K_oo: where an fp64 LAPACK solve (numpy)
-from the oracle's R rounded to fp64 itself misses the oracle's K_oo by more than 1e-11, the GPU K_oo
-may exceed 1e-10 but must stay within 10x of that LAPACK error (next to an R pole, the rounding of
-the pole term of an fp64 R already costs ~1e-10 in K_oo). Every exclusion is printed and counted.
-|T|^2 and the row sums have no exclusion. PAPER.md:128-130, 152-153 (§3: the fine mesh exists to
-resolve narrow resonances, so near-pole energies are the workload).
+1e-8. The only exclusion is reading T4's fp64 floor for K_oo: next to an R pole or a pole of K the
+matching is so ill-conditioned (scaled cond_1(A) up to 1e9) that an fp64-accurate R (normwise error
+~1e-15 .. 1e-14) already costs ~1e-10 in K_oo. There the GPU K_oo may exceed 1e-10 only if an fp64
+LAPACK solve (numpy) fed the same R misses the oracle's K_oo by a comparable amount (within 10x, and
+that miss itself above 1e-11), while the GPU R stays within 1e-13 of the oracle's. Every exclusion is
+printed and counted. |T|^2 and the row sums have no exclusion. PAPER.md:128-130, 152-153 (§3: the fine
+mesh exists to resolve narrow resonances, so near-pole energies are the workload).
 """
 import time
 
@@ -36,22 +37,24 @@ def scaled_cond(R, G, Gp, a):
     return float(np.linalg.cond(A / np.max(np.abs(A), axis=0)[None, :], 1))
 
 
-def lapack_floor(s, p):
-    """Normwise K_oo error of an fp64 LAPACK solve (numpy) from the oracle's R rounded to fp64: the
-    accuracy any fp64 matching of this R can be expected to reach (reading T4)."""
-    c, o, R = s["c"], int(s["no"][p]), s["ref"]["R"][p]
+def lapack_floor(s, p, R):
+    """Normwise K_oo error against the oracle of an fp64 LAPACK solve (numpy) fed the fp64 R `R`: what
+    any fp64 matching of this R can be expected to reach (reading T4)."""
+    c, o = s["c"], int(s["no"][p])
     A = np.diag(s["G"][p]) - c.a * R * s["Gp"][p][None, :]
     B = np.diag(s["F"][p]) - c.a * R * s["Fp"][p][None, :]
     return nrel(-np.linalg.solve(A, B[:, :o])[:o], s["ref"]["K"][p][:o, :o])
 
 
-def check_K(s, p, ek, excl):
-    """K_oo bar with reading T4's fp64-floor exclusion (printed and counted by the caller)."""
+def check_K(s, p, ek, R, excl):
+    """K_oo bar with reading T4's fp64-floor exclusion (printed and counted by the caller); R = the fp64
+    R the GPU matching was fed (its own R end to end, the oracle's rounded R stage by stage)."""
     if ek < TOL_K:
         return
-    enp = lapack_floor(s, p)
-    assert enp > 0.1 * TOL_K and ek < 10.0 * enp, (s["lab"][p], ek, enp)
-    excl.append((s["lab"][p], f"{ek:.2e}", f"lapack {enp:.2e}"))
+    er = nrel(R, s["ref"]["R"][p])
+    enp = lapack_floor(s, p, R)
+    assert er < 1e-13 and enp > 0.1 * TOL_K and ek < 10.0 * enp, (s["lab"][p], ek, enp, er)
+    excl.append((s["lab"][p], f"{ek:.2e}", f"lapack(same R) {enp:.2e}"))
 
 
 @pytest.fixture(scope="module", params=["darc", "fine"])
@@ -98,7 +101,7 @@ def _check_end_to_end(s, res, what):
         kap = scaled_cond(ref["R"][p], s["G"][p], s["Gp"][p], c.a) if o else 0.0
         rows.append((s["lab"][p], o, er, ek, et, es, kap))
         assert er < TOL_R, (s["lab"][p], er)
-        check_K(s, p, ek, excl)
+        check_K(s, p, ek, res["R"][p], excl)
         assert et < TOL_T2 and es < TOL_T2, (s["lab"][p], et, es)
     print(f"\n[{c.name} {what}] label, n_open, err R, err K_oo, err |T|^2, err rowsum, scaled cond(A)")
     for r in rows:
@@ -138,7 +141,7 @@ def test_sample_stagewise(sample):
         o = int(no[p])
         ek = nrel(K[p][:o, :o], ref["K"][p][:o, :o]) if o else 0.0
         et, es = nrel(T2[p], ref["T2"][p]), nrel(rs[p], ref["rowsum"][p])
-        check_K(sample, p, ek, excl)
+        check_K(sample, p, ek, ref["R"][p], excl)
         assert et < TOL_T2 and es < TOL_T2, (sample["lab"][p], et, es)
         worst = [max(worst[0], ek), max(worst[1], et), max(worst[2], es)]
     print(f"\n[{c.name} stagewise] worst K_oo {worst[0]:.1e}  |T|^2 {worst[1]:.1e}  rowsum {worst[2]:.1e}; "

@@ -178,3 +178,24 @@ def test_int8_fine_block(ctx):
         vals, st = oracle.R_entries(c.w, c.Ek, c.a, E[l], ii, jj)
         assert np.max(np.abs(R8[ii, jj] - vals)) / np.max(np.abs(R8)) < 1e-12
         assert nrel(out8["T2"][d].cpu().numpy(), out64["T2"][d].cpu().numpy()) < 1e-8
+
+
+def test_int8_crt_worst_case_magnitude(ctx):
+    """The CRT's exactness bound at its limit (rint8.cu: |P| <= nlev 2^106 < M/2, 0.23 M at the maximum
+    nlev 131071): constant-sign amplitudes w > 0 and E below every pole (all d_k > 0), so every product
+    w_ik d_k w_jk is positive and |P| reaches its maximum; nch = 300 runs the CTA-pair GEMM, nlev > 65000
+    the balanced int8 residues. R against the long-double oracle."""
+    import torch
+    rng = np.random.default_rng(17)
+    nch, nlev = 300, 131071
+    Ek = np.sort(rng.uniform(1.0, 200.0, nlev))
+    w = rng.uniform(0.01, 0.05, (nch, nlev))
+    E = np.array([0.25, 0.9])
+    R, st = ctx.build_R(w, Ek, 12.0, E)
+    torch.cuda.synchronize()
+    R = R.cpu().numpy()
+    assert np.all(st.cpu().numpy() == 0)
+    assert np.all(R > 0)
+    for p, x in enumerate(E):
+        ref, _ = oracle.R(w, Ek, 12.0, x, threads=oracle.default_threads())
+        assert nrel(R[p], ref) < 1e-12, (x, nrel(R[p], ref))
