@@ -1,8 +1,8 @@
 // match.cu - S3+S4 of the sweep: K = -(G - aRG')^{-1}(F - aRF')   (BASELINE.json:5).
 // The paper is silent on this step (PAPER.md:459-514 stops at R); DESIGN.md §5.2 gives the design:
 // one CTA per energy (persistent over energies, workspace slot = blockIdx.x), blocked right-looking
-// LU with partial pivoting of A on the augmented matrix [A | B_open] (outer blocks of 64 built from
-// two 32-wide panels, FP64 DMMA trailing updates through the TMA pipeline of cta_la.cuh), then
+// LU with partial pivoting of A on the augmented matrix [A | B_open] (outer blocks of 256 built from
+// 32-wide panels, FP64 DMMA trailing updates through the TMA pipeline of cta_la.cuh), then
 // blocked back substitution; only the n_open open columns of B are solved, closed columns of K
 // are -e_j (precondition of rmx.h; SURVEY §8(c) reading 9).
 #include "cta_la.cuh"
@@ -121,42 +121,58 @@ __global__ void __launch_bounds__(NT, 1)
 
     PH_MARK(0);  // formation pass
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
-    // Outer blocks of W = NB = 128 columns, factored as four 32-wide panels (each followed by a
-    // K = 32 update of the block's remaining columns), then U12 = L11^{-1} A12 as ONE in-place DMMA
-    // GEMM with the explicit 128 x 128 inverse (one 128-row tile row), then the K = 128 trailing
-    // update.
+    // Outer blocks of 256 columns made of two 128-wide sub-blocks a, b. A sub-block is factored as
+    // four 32-wide panels (each followed by a K = 32 update of the sub-block's remaining columns);
+    // U12a = L11a^{-1} A12 as ONE in-place DMMA GEMM with the explicit 128 x 128 inverse (one
+    // 128-row tile row) over every column right of a; sub-block b's columns are updated and factored
+    // (its row interchanges run over the whole block, L21a included, while the trailing columns of
+    // all rows below a still wait for a's update), b's U rows get a's update and U12b; then ONE
+    // trailing update with K = 256 (C read and written once per 256 columns instead of twice).
     int singular = 0;
-    for (int P0 = 0; P0 < n; P0 += NB) {
-      const int W = min(NB, n - P0);
-      for (int q0 = 0; q0 < W; q0 += PB) {
-        const int c = P0 + q0, wq = min(PB, W - q0), rem = W - q0 - wq;
-        singular |= panel_lu(Mw, ldm, n, c, wq, P0, ncols, sm.ipiv + q0, sm.gemm, sm.ubuf, sm.redv,
+    auto factor_sub = [&](int c0, int Wblk, int sc0) {
+      for (int q0 = 0; q0 < Wblk; q0 += PB) {
+        const int c = c0 + q0, wq = min(PB, Wblk - q0), rem = Wblk - q0 - wq;
+        singular |= panel_lu(Mw, ldm, n, c, wq, sc0, ncols, sm.ipiv + q0, sm.gemm, sm.ubuf, sm.redv,
                              sm.redi);
         if (rem > 0) {
-          // block columns right of this panel: U rows = L_qq^{-1} A ; rows below -= L U
+          // sub-block columns right of this panel: U rows = L_qq^{-1} A ; rows below -= L U
           tri_inv64(Mw, ldm, c, wq, TRI_UNIT_LOWER, sm.tri, Tv.base, TG);
           gemm_set(wq, rem, wq, opk(Tv, 0, 0), opn(Mv, c, c + wq), Mv, c, c + wq, false, 0.0, smg, gs);
           gemm_sub(n - c - wq, rem, wq, opk(Mv, c + wq, c), opn(Mv, c, c + wq), Mv, c + wq, c + wq,
                    false, smg, gs);
         }
       }
-      PH_MARK(1);  // panels (panel_lu + in-block K = 32 updates)
+    };
+    for (int P0 = 0; P0 < n; P0 += 2 * NB) {
+      const int W = min(2 * NB, n - P0), Wa = min(NB, W), Wb = W - Wa, ca = P0 + Wa;
       // trailing columns (A part and right-hand sides); when the last block ends on an odd n the
       // zero pad column n is skipped so that every C row stays 16-byte aligned
       const int ct = min((P0 + W + 1) & ~1, ncols);
       const int nt = ncols - ct;
-      if (nt > 0) {
+      factor_sub(P0, Wa, P0);
+      PH_MARK(1);  // panels (panel_lu + in-block K = 32 updates)
+      if (Wb == 0 && nt == 0) continue;
+      tri_inv128(Mv, P0, Wa, TRI_UNIT_LOWER, Tv, smg, gs);  // L11a^{-1}
+      PH_MARK(5);
+      const int c2 = Wb > 0 ? ca : ct;  // ca = P0 + 128 is even when Wb > 0
+      gemm_set(Wa, ncols - c2, Wa, opk(Tv, 0, 0), opn(Mv, P0, c2), Mv, P0, c2, false, 0.0, smg, gs);
+      PH_MARK(2);
+      if (Wb > 0) {
+        gemm_sub(n - ca, Wb, Wa, opk(Mv, ca, P0), opn(Mv, P0, ca), Mv, ca, ca, false, smg, gs);
         PH_MARK(2);
-        tri_inv128(Mv, P0, W, TRI_UNIT_LOWER, Tv, smg, gs);  // L11^{-1}
-        PH_MARK(5);
-        // U12 = L11^{-1} A12 in place: W <= 128 = BM rows, so each output tile column depends only
-        // on its own input columns
-        gemm_set(W, nt, W, opk(Tv, 0, 0), opn(Mv, P0, ct), Mv, P0, ct, false, 0.0, smg, gs);
-        if (P0 + W < n)
-          gemm_sub(n - P0 - W, nt, W, opk(Mv, P0 + W, P0), opn(Mv, P0, ct), Mv, P0 + W, ct, false,
-                   smg, gs);
+        factor_sub(ca, Wb, P0);
+        PH_MARK(1);
+        if (nt > 0) {
+          gemm_sub(Wb, nt, Wa, opk(Mv, ca, P0), opn(Mv, P0, ct), Mv, ca, ct, false, smg, gs);
+          PH_MARK(2);
+          tri_inv128(Mv, ca, Wb, TRI_UNIT_LOWER, Tv, smg, gs);  // L22b^{-1}
+          PH_MARK(5);
+          gemm_set(Wb, nt, Wb, opk(Tv, 0, 0), opn(Mv, ca, ct), Mv, ca, ct, false, 0.0, smg, gs);
+        }
       }
-      PH_MARK(2);  // U12 + K = 128 trailing update
+      if (nt > 0 && P0 + W < n)
+        gemm_sub(n - P0 - W, nt, W, opk(Mv, P0 + W, P0), opn(Mv, P0, ct), Mv, P0 + W, ct, false, smg, gs);
+      PH_MARK(2);  // U12 + K = 256 trailing update
     }
 
     // ---- S4b: blocked back substitution U Y = L^{-1} P B_open (Y = columns [npad, npad+o)) ----
