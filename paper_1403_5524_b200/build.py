@@ -22,10 +22,10 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 LIBS = ["-L/usr/local/cuda/lib64", "-lcusolver", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(os.path.dirname(PKG), "include", "rmx.h"))
     deps.append(os.path.abspath(__file__))
@@ -36,6 +36,20 @@ def build_phases(verbose: bool = False) -> str:
     """Diagnostic variant with per-phase clock64 counters in the matching kernel (librmx_phases.so)."""
     out = os.path.join(PKG, "librmx_phases.so")
     cmd = [NVCC, *FLAGS, "-DRMX_PHASES", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd, cwd=CSRC)
+    return out
+
+
+def build_checked(force: bool = False, verbose: bool = False) -> str:
+    """Bounds-checked variant (librmx_checked.so, -DRMX_CHECKS): device-side index / extent checks
+    that trap (rmx_common.cuh RMX_CHECK) - the stand-in for compute-sanitizer, which is closed on
+    the GPU pool (tests/test_gpu_checked.py)."""
+    out = os.path.join(PKG, "librmx_checked.so")
+    if not force and os.path.exists(out) and not _stale(out):
+        return out
+    cmd = [NVCC, *FLAGS, "-DRMX_CHECKS", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd, cwd=CSRC)
@@ -57,6 +71,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 if __name__ == "__main__":
     if "--phases" in sys.argv:
         print(build_phases(verbose=True))
+    elif "--checked" in sys.argv:
+        print(build_checked(force=True, verbose=True))
     else:
         build(force="--force" in sys.argv, verbose=True)
         print(LIB)

@@ -49,9 +49,12 @@ struct MatView {
   const CUtensorMap *tm;
   double *base;
   int64_t ld;
+  int64_t rows = 0;  // rows of the allocation (bounds-checked build; 0 = unchecked)
   __device__ __forceinline__ double *at(int r, int c) const {
+    RMX_CHECK(r >= 0 && c >= 0 && c < ld && (rows == 0 || r < rows));
     return base + static_cast<int64_t>(r) * ld + c;
   }
+  __device__ __forceinline__ const double *end() const { return rows ? base + rows * ld : nullptr; }
 };
 // An operand: the submatrix of `v` starting at (r0, c0). kc: element (i, k) of the operand is
 // v(r0 + i, c0 + k) (k contiguous); otherwise v(r0 + k, c0 + i).
@@ -116,6 +119,7 @@ struct GemmArgs {
   int nseg = 1;
   bool neg2 = false;
   double alpha = 1.0;  // set mode (read_c false): C = alpha (A.B) + diag_add I
+  const double *c_end = nullptr;  // one past C's allocation (bounds-checked build; nullptr = unchecked)
 };
 
 // C[M x N] op= A[M x K] . B[K x N] on the calling CTA (all NT threads call it).
@@ -176,6 +180,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
         const uint32_t rb = round16(cols * 8);
         if (lane == 0) mbar_arrive_expect_tx(&gs->cfull, rb * rows);
         __syncwarp();
+        RMX_CHECK(!ga.c_end || ga.C + static_cast<int64_t>(tm * BM + rows - 1) * ga.ldc + tn * BN + cols <= ga.c_end);
         bulk_rows(Cs, CS_LD, ga.C + static_cast<int64_t>(tm * BM) * ga.ldc + tn * BN, ga.ldc, rows,
                   rb, &gs->cfull);
       }
@@ -365,6 +370,7 @@ static __device__ __noinline__ void gemm_impl(const GemmArgs &gar, uint8_t *smem
         const int r = tm * BM + wm * WTM + mi * 8 + arow;
         if (r >= M) continue;
         double *crow = ga.C + static_cast<int64_t>(r) * ga.ldc;
+        RMX_CHECK(!ga.c_end || crow + min(N, tn * BN + BN) <= ga.c_end);
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
@@ -409,6 +415,7 @@ __device__ __forceinline__ void gemm_sub(int M, int N, int K, const Op &a, const
                                          const MatView &c, int cr0, int cc0, bool lower,
                                          double *smem, GemmSync *gs) {
   GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, true, false, 0.0};
+  ga.c_end = c.end();
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 // C = A.B + diag_add I
@@ -416,6 +423,7 @@ __device__ __forceinline__ void gemm_set(int M, int N, int K, const Op &a, const
                                          const MatView &c, int cr0, int cc0, bool lower,
                                          double diag_add, double *smem, GemmSync *gs) {
   GemmArgs ga{a, b, c.at(cr0, cc0), c.ld, M, N, K, lower, false, false, diag_add};
+  ga.c_end = c.end();
   gemm_rt(ga, gemm_smem_align(smem), gs);
 }
 // ------------------------------------------------------------------------------------------------
@@ -516,6 +524,7 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
     // 4. the sub-panel's interchanges, in order, on the rest of the augmented rows
     for (int jj = 0; jj < w; ++jj) {
       const int pr = ipiv[s0 + jj], j = c0 + jj;
+      RMX_CHECK(pr >= j && pr < n && sc1 <= ld);
       if (pr != j) {
         double *ra = M + static_cast<int64_t>(j) * ld;
         double *rb = M + static_cast<int64_t>(pr) * ld;

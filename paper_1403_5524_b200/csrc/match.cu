@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(NT, 1)
   const MatchLayout L = match_layout(n);
   const int ldm = static_cast<int>(L.ldm), npad = static_cast<int>(L.npad);
   double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
-  const MatView Mv{views + (blockIdx.x * 2 + 0) * NVIEW, slot + L.m_off, ldm};
-  const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, TG};
+  const MatView Mv{views + (blockIdx.x * 2 + 0) * NVIEW, slot + L.m_off, ldm, n};
+  const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, TG, TG};
   double *Mw = Mv.base;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;

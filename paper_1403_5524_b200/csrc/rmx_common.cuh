@@ -2,6 +2,7 @@
 // FP64 tensor-core MMA (DMMA), cp.async, mbarrier and TMA (cp.async.bulk.tensor) wrappers.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda.h>
 
@@ -12,6 +13,24 @@
 namespace rmx {
 
 constexpr double kPoleGuard = 1e-10;  // |E - E_k| < 1e-10 Ry -> RMX_E_POLE
+
+// Device-side bounds checks of the bounds-checked build (python -m paper_1403_5524_b200.build
+// --checked -> librmx_checked.so, -DRMX_CHECKS; tests/test_gpu_checked.py): a failed check prints its
+// place and traps, which the host sees as a CUDA error. Compiled out of librmx.so.
+#ifdef RMX_CHECKS
+#define RMX_CHECK(cond)                                                                          \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("RMX_CHECK(%s) failed at %s:%d block %d thread %d\n", #cond, __FILE__, __LINE__,   \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                       \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define RMX_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 // ---- nearest pole ----------------------------------------------------------------------------
 // Index k* of the pole nearest to E (E_k ascending, the rmx.h precondition; ties -> lower index).

@@ -190,6 +190,7 @@ __device__ __forceinline__ void cgemm(int M, int N, int K, const Op &are, const 
   g.nseg = 2;
   g.neg2 = true;
   g.alpha = alpha;
+  g.c_end = cr.end();
   gemm_rt(g, gemm_smem_align(smem), gs);
   // Im = Ar.Bi + Ai.Br
   g.b = bim;
@@ -197,6 +198,7 @@ __device__ __forceinline__ void cgemm(int M, int N, int K, const Op &are, const 
   g.neg2 = false;
   g.C = ci.at(r0, c0);
   g.ldc = ci.ld;
+  g.c_end = ci.end();
   gemm_rt(g, gemm_smem_align(smem), gs);
 }
 
@@ -213,11 +215,11 @@ __global__ void __launch_bounds__(NT, 1)
   const int ldo = static_cast<int>(L.ldo);
   double *slot = ws + static_cast<int64_t>(blockIdx.x) * ws_slot;
   const CUtensorMap *vw = views + blockIdx.x * 5 * NVIEW;
-  const MatView Arv{vw + 0 * NVIEW, slot + L.ar_off, ldo};
-  const MatView Aiv{vw + 1 * NVIEW, slot + L.ai_off, ldo};
-  const MatView Yrv{vw + 2 * NVIEW, slot + L.yr_off, ldo};
-  const MatView Yiv{vw + 3 * NVIEW, slot + L.yi_off, ldo};
-  const MatView Pv{vw + 4 * NVIEW, slot + L.p_off, ldo};
+  const MatView Arv{vw + 0 * NVIEW, slot + L.ar_off, ldo, n};
+  const MatView Aiv{vw + 1 * NVIEW, slot + L.ai_off, ldo, n};
+  const MatView Yrv{vw + 2 * NVIEW, slot + L.yr_off, ldo, n};
+  const MatView Yiv{vw + 3 * NVIEW, slot + L.yi_off, ldo, n};
+  const MatView Pv{vw + 4 * NVIEW, slot + L.p_off, ldo, n};
   double *dr = slot + L.d_off, *di = dr + n, *vv = di + n;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(NT, 1)
       // rows >= their first row or other columns (row-major tile order).
       {
         GemmArgs g{opn(Arv, 0, 0), opn(Yrv, 0, 0), Pv.base, Pv.ld, o, o, o, true, false, false, 0.0, 1};
+        g.c_end = Pv.end();
         g.a2 = opn(Aiv, 0, 0);
         g.b2 = opn(Yiv, 0, 0);
         g.nseg = 2;
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(NT, 1)
         g.b2 = opn(Yrv, 0, 0);
         g.neg2 = false;
         g.C = Yiv.base;
+        g.c_end = Yiv.end();
         gemm_rt(g, gemm_smem_align(smg), gs);
       }
       TPH_MARK(6);  // Y = D^{-1} Z and A^{-1} = Z^T Y
