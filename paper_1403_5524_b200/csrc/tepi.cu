@@ -25,8 +25,9 @@
 //   5. mirror, |T_ij|^2 = 4 (Im^2 + (delta_ij - Re)^2), row sums in a fixed order (deterministic)
 // Executed flops ~ 4 o^3 (SURVEY §8(d) counts (16/3) o^3 as algorithmic).
 // |T|^2 and the row sums are invariant under K -> -K (A -> conj(A)).
-#include "cta_la.cuh"
+#include "cta_cgemm.cuh"
 #include "rmx_internal.h"
+#include <cstdlib>
 
 namespace rmx {
 
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(NT, 1)
     tepi_kernel(const double *K, int64_t ldk, int64_t kstride, int n, int64_t ne,
                 const int32_t *__restrict__ n_open, double *T2, const int64_t *t2_slot,
                 double *rowsum, LevelSums lv, PhotoArgs pa, double *ws, int64_t ws_slot,
-                const CUtensorMap *views, int32_t *status) {
+                const CUtensorMap *views, int32_t *status, int c4m) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TepiSmem &sm = *reinterpret_cast<TepiSmem *>(smem_raw);
   const TepiLayout L = tepi_layout(n);
@@ -223,6 +224,16 @@ __global__ void __launch_bounds__(NT, 1)
   double *dr = slot + L.d_off, *di = dr + n, *vv = di + n;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
+  // complex products: 3M single pass (cta_cgemm.cuh, default) or the 4-product two-pass form
+  // (RMX_TEPI_4M, an A/B switch)
+  auto cg = [&](int M, int N, int K, const Op &are, const Op &aim, const Op &bre, const Op &bim,
+                const MatView &cr, const MatView &ci, int r0, int c0, bool lower, bool sub, double alpha,
+                int kband) {
+    if (c4m)
+      cgemm(M, N, K, are, aim, bre, bim, cr, ci, r0, c0, lower, sub, alpha, kband, smg, gs);
+    else
+      cgemm3(M, N, K, are, aim, bre, bim, cr, ci, r0, c0, lower, sub, alpha, kband, smg, gs);
+  };
 
   for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
     int o = n_open ? n_open[e] : n;
@@ -281,21 +292,21 @@ __global__ void __launch_bounds__(NT, 1)
         TPH_MARK(1);  // diagonal blocks
         if (mb > 0) {
           // W21 = A21 T1^T (= L21 D1) for all rows below sub-block 1
-          cgemm(mb, W1, W1, opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0), opk(Arv, P0, P0), opk(Aiv, P0, P0),
-                Yrv, Yiv, 0, 0, false, false, 1.0, 0, smg, gs);
+          cg(mb, W1, W1, opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0), opk(Arv, P0, P0), opk(Aiv, P0, P0),
+             Yrv, Yiv, 0, 0, false, false, 1.0, 0);
           TPH_MARK(2);  // W21 = A21 Tinv^T
           scale_cols(Yrv, Yiv, 0, 0, Arv, Aiv, P0 + W1, P0, mb, W1, dr + P0, di + P0, sm.tri);
           TPH_MARK(3);  // L21 scaling
           if (W2 > 0) {
             // sub-block 2's columns: A[P0+W1:, P0+W1:P0+W] -= W21 L21[0:W2]^T
-            cgemm(mb, W2, W1, opk(Yrv, 0, 0), opk(Yiv, 0, 0), opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0),
-                  Arv, Aiv, P0 + W1, P0 + W1, false, true, 1.0, 0, smg, gs);
+            cg(mb, W2, W1, opk(Yrv, 0, 0), opk(Yiv, 0, 0), opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0),
+               Arv, Aiv, P0 + W1, P0 + W1, false, true, 1.0, 0);
             TPH_MARK(4);
             diag_ldlt_inv(Arv, Aiv, P0 + W1, W2, dr, di, sm.tri);
             TPH_MARK(1);
             if (m > 0) {
-              cgemm(m, W2, W2, opk(Arv, P0 + W, P0 + W1), opk(Aiv, P0 + W, P0 + W1), opk(Arv, P0 + W1, P0 + W1),
-                    opk(Aiv, P0 + W1, P0 + W1), Yrv, Yiv, W2, W1, false, false, 1.0, 0, smg, gs);
+              cg(m, W2, W2, opk(Arv, P0 + W, P0 + W1), opk(Aiv, P0 + W, P0 + W1), opk(Arv, P0 + W1, P0 + W1),
+                 opk(Aiv, P0 + W1, P0 + W1), Yrv, Yiv, W2, W1, false, false, 1.0, 0);
               TPH_MARK(2);
               scale_cols(Yrv, Yiv, W2, W1, Arv, Aiv, P0 + W, P0 + W1, m, W2, dr + P0 + W1, di + P0 + W1, sm.tri);
               TPH_MARK(3);
@@ -303,8 +314,8 @@ __global__ void __launch_bounds__(NT, 1)
           }
           if (m > 0) {
             // A22 -= [W21 W22] [L21 L22]^T (lower tiles), K = W per product
-            cgemm(m, m, W, opk(Yrv, W2, 0), opk(Yiv, W2, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0),
-                  Arv, Aiv, P0 + W, P0 + W, true, true, 1.0, 0, smg, gs);
+            cg(m, m, W, opk(Yrv, W2, 0), opk(Yiv, W2, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0),
+               Arv, Aiv, P0 + W, P0 + W, true, true, 1.0, 0);
             TPH_MARK(4);  // trailing updates
           }
         }
@@ -320,17 +331,17 @@ __global__ void __launch_bounds__(NT, 1)
             *Aiv.at(R0 + q / W2, R0 + CB + q % W2) = 0.0;
           }
           // Tinv_128 = [[T1, 0], [-T2 L21 T1, T2]]: Q1 = L21 T1 -> Y, then -T2 Q1 over L21
-          cgemm(W2, CB, CB, opk(Arv, R0 + CB, R0), opk(Aiv, R0 + CB, R0), opn(Arv, R0, R0), opn(Aiv, R0, R0),
-                Yrv, Yiv, 0, 0, false, false, 1.0, 0, smg, gs);
-          cgemm(W2, CB, W2, opk(Arv, R0 + CB, R0 + CB), opk(Aiv, R0 + CB, R0 + CB), opn(Yrv, 0, 0),
-                opn(Yiv, 0, 0), Arv, Aiv, R0 + CB, R0, false, false, -1.0, 0, smg, gs);
+          cg(W2, CB, CB, opk(Arv, R0 + CB, R0), opk(Aiv, R0 + CB, R0), opn(Arv, R0, R0), opn(Aiv, R0, R0),
+             Yrv, Yiv, 0, 0, false, false, 1.0, 0);
+          cg(W2, CB, W2, opk(Arv, R0 + CB, R0 + CB), opk(Aiv, R0 + CB, R0 + CB), opn(Yrv, 0, 0),
+             opn(Yiv, 0, 0), Arv, Aiv, R0 + CB, R0, false, false, -1.0, 0);
         }
         if (R0 > 0) {
           // Tt = L_{B,0:R0} Z_{0:R0,0:R0} -> Y (Z lower triangular: kband 2); Z_B = -Tinv_128 Tt
-          cgemm(W, R0, R0, opk(Arv, R0, 0), opk(Aiv, R0, 0), opn(Arv, 0, 0), opn(Aiv, 0, 0), Yrv, Yiv, 0, 0,
-                false, false, 1.0, 2, smg, gs);
-          cgemm(W, R0, W, opk(Arv, R0, R0), opk(Aiv, R0, R0), opn(Yrv, 0, 0), opn(Yiv, 0, 0), Arv, Aiv, R0,
-                0, false, false, -1.0, 0, smg, gs);
+          cg(W, R0, R0, opk(Arv, R0, 0), opk(Aiv, R0, 0), opn(Arv, 0, 0), opn(Aiv, 0, 0), Yrv, Yiv, 0, 0,
+             false, false, 1.0, 2);
+          cg(W, R0, W, opk(Arv, R0, R0), opk(Aiv, R0, R0), opn(Yrv, 0, 0), opn(Yiv, 0, 0), Arv, Aiv, R0,
+             0, false, false, -1.0, 0);
         }
       }
       TPH_MARK(5);  // Z = L^{-1}
@@ -359,7 +370,7 @@ __global__ void __launch_bounds__(NT, 1)
       // 4. A^{-1} = Z^T Y (lower tiles; A(i,k) = Z(k,i) = 0 for k < i: kband 1). Re -> P, then Im
       // in place over Y_i: an output tile is stored after its own reads, and later tiles read only
       // rows >= their first row or other columns (row-major tile order).
-      {
+      if (c4m) {
         GemmArgs g{opn(Arv, 0, 0), opn(Yrv, 0, 0), Pv.base, Pv.ld, o, o, o, true, false, false, 0.0, 1};
         g.c_end = Pv.end();
         g.a2 = opn(Aiv, 0, 0);
@@ -373,6 +384,10 @@ __global__ void __launch_bounds__(NT, 1)
         g.C = Yiv.base;
         g.c_end = Yiv.end();
         gemm_rt(g, gemm_smem_align(smg), gs);
+      } else {
+        // one pass: Re -> P, Im in place over Y_i (each tile stores after its own reads)
+        cgemm3(o, o, o, opn(Arv, 0, 0), opn(Aiv, 0, 0), opn(Yrv, 0, 0), opn(Yiv, 0, 0), Pv, Yiv, 0, 0, true,
+               false, 1.0, 1, smg, gs);
       }
       TPH_MARK(6);  // Y = D^{-1} Z and A^{-1} = Z^T Y
       // 5. symmetric A^{-1}: upper triangles from the lower ones
@@ -482,6 +497,22 @@ extern "C" int rmx_debug_tepi_phases(unsigned long long *out) {
 }
 #endif
 
+#ifdef RMX_CHECKS
+// Self-test of the bounds-checked build: an index one row past a 4 x 4 view must trap.
+__global__ void checks_selftest_kernel(double *buf, int row) {
+  const MatView v{nullptr, buf, 4, 4};
+  *v.at(row, 0) = 1.0;
+}
+extern "C" int rmx_debug_checks_selftest(int row) {
+  double *buf = nullptr;
+  if (cudaMalloc(&buf, 64 * sizeof(double)) != cudaSuccess) return -1;
+  checks_selftest_kernel<<<1, 1>>>(buf, row);
+  const cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(buf);
+  return static_cast<int>(e);
+}
+#endif
+
 int64_t tepi_ws_doubles_per_slot(int64_t nch) { return tepi_layout(nch).slot; }
 
 // Matrices of one slot whose TMA descriptors the kernel uses: (Ar, Ai, Yr, Yi, P), NVIEW boxes each.
@@ -499,8 +530,9 @@ cudaError_t launch_tepi(const double *K, int64_t ldk, int64_t kstride, int64_t n
   cudaError_t ce = ensure_smem_attr(reinterpret_cast<const void *>(tepi_kernel), sizeof(TepiSmem));
   if (ce != cudaSuccess) return ce;
   const int grid = static_cast<int>(ne < ws_slots ? ne : ws_slots);
+  static const int c4m = getenv("RMX_TEPI_4M") != nullptr;  // A/B switch: 4-product complex GEMMs
   tepi_kernel<<<grid, NT, sizeof(TepiSmem), st>>>(K, ldk, kstride, static_cast<int>(nch), ne, n_open,
-                                                  T2, t2_slot, rowsum, lv, pa, ws, ws_slot, views, status);
+                                                  T2, t2_slot, rowsum, lv, pa, ws, ws_slot, views, status, c4m);
   return cudaGetLastError();
 }
 
