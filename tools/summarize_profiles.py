@@ -76,7 +76,11 @@ if os.path.exists(rep):
             f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(units.get(m), None)
             if f and ent[m] is not None and ent[m] == ent[m]:
                 ent[m.replace(".sum", ".bytes")] = ent[m] * f
-        ent["workload"] = {"config": "darc", "energies_per_launch": 296}
+        if "oz_" in name:  # INT8-CRT kernels: one launch = one chunk of 8 energies (kInt8Chunk at darc)
+            ent["workload"] = {"config": "darc", "energies_per_launch": 8,
+                               "note": "one launch = one chunk of 8 energies (x 16 moduli)"}
+        else:
+            ent["workload"] = {"config": "darc", "energies_per_launch": 296}
         res.setdefault(name, ent)
     path = os.path.join(out_dir, f"r{rnd}_ncu_kernels.json")
     old = json.load(open(path)) if os.path.exists(path) else {}
