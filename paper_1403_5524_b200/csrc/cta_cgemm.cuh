@@ -5,10 +5,11 @@
 // operand planes (the 2-pass real form loaded every operand twice).
 // Same pipeline as cta_la.cuh gemm_impl (one TMA producer warp, 8 DMMA consumer warps, mbarrier
 // ring, swizzled fragment loads); tile 128 x 32 with 32 x 16 warp tiles so that the three
-// accumulator sets (48 registers) fit the 168-register budget of a 9-warp CTA; the sum operands
-// (Ar + Ai), (Br + Bi) are formed in registers. Set mode (C = alpha A.B): 2 stages of 80 KB. Sub mode
-// (C -= A.B, the trailing updates): 3 stages of 40 KB and both C planes of a tile staged through
-// shared memory by the producer while the tile's k loop runs (C3Cfg).
+// accumulator sets (48 registers) fit the 168-register budget of a 9-warp CTA; 2 stages of 80 KB
+// (the four planes' k-slices); the sum operands (Ar + Ai), (Br + Bi) are formed in registers. The
+// T epilogue uses it for the products that write C (C = alpha A.B); its sub mode (C -= A.B, C read in
+// the epilogue) is kept for completeness - the trailing updates run the 4-product form of gemm_impl,
+// whose 128 x 64 tiles amortise the staged C tile over twice the k range (tepi.cu).
 // Rounding: Im = (T3 - T1) - T2; the error bound u (|Ar| + |Ai|)(|Br| + |Bi|) is that of the
 // 4-product form up to a factor <= 2 (normwise).
 #pragma once
@@ -18,20 +19,10 @@ namespace rmx {
 namespace la {
 
 constexpr int C3_BN = 32, C3_WTN = C3_BN / WN, C3_NI = C3_WTN / 8;  // 32 x 16 warp tiles, 4 x 2 fragments
-// Pipeline shape per mode: set (C = alpha A.B): k-slices of 32, 2 stages of 80 KB; sub (C -= A.B, both
-// operands k-contiguous - the trailing updates): k-slices of 16, 3 stages of 40 KB plus both C planes
-// of the next tile staged through shared memory (bulk row copies issued while the tile's k loop runs,
-// read in the epilogue).
-template <bool SUB>
-struct C3Cfg {
-  static constexpr int BKX = SUB ? 16 : 32, NST = SUB ? 3 : 2;
-  static constexpr int A_BYTES = BM * BKX * 8, B_BYTES = C3_BN * BKX * 8;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // Ar, Ai, Br, Bi
-  static constexpr int CS_LD = C3_BN + 2, CS_PLANE = BM * CS_LD;
-  static constexpr int SMEM = 1024 + NST * STAGE_BYTES + (SUB ? 2 * CS_PLANE * 8 : 0);
-  static_assert(SMEM <= GEMM_SMEM_BYTES, "cgemm3 stages exceed the gemm smem");
-  static_assert(NST <= STAGES, "GemmSync has STAGES barriers");
-};
+constexpr int C3_STAGES = 2;
+constexpr int C3_A_BYTES = BM * BK * 8, C3_B_BYTES = C3_BN * BK * 8;
+constexpr int C3_STAGE_BYTES = 2 * C3_A_BYTES + 2 * C3_B_BYTES;  // Ar, Ai, Br, Bi
+static_assert(1024 + C3_STAGES * C3_STAGE_BYTES <= GEMM_SMEM_BYTES, "cgemm3 stages exceed the gemm smem");
 
 struct CGemmArgs {
   Op ar, ai, br, bi;  // operands (re, im planes); a pair shares its layout flag
@@ -48,36 +39,30 @@ __device__ __forceinline__ int c3_tiles_in_row(int tm, int tiles_n, bool lower) 
   if (!lower) return tiles_n;
   return min(tiles_n, (tm * BM + BM - 1) / C3_BN + 1);
 }
-__device__ __forceinline__ int c3_kc_first(int kband, int tm, int tn, int bk) {
-  return kband == 1 ? (tm * BM) / bk : (kband == 2 ? (tn * C3_BN) / bk : 0);
+__device__ __forceinline__ int c3_kc_first(int kband, int tm, int tn) {
+  return kband == 1 ? (tm * BM) / BK : (kband == 2 ? (tn * C3_BN) / BK : 0);
 }
 
-template <bool A_KC, bool B_KC, bool SUB>
+template <bool A_KC, bool B_KC>
 static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *smem_al, GemmSync *gs) {
-  using CF = C3Cfg<SUB>;
-  constexpr int BKX = CF::BKX, NST = CF::NST;
-  static_assert(!SUB || (A_KC && B_KC), "sub mode: k-contiguous operands only");
   // the argument block arrives by reference (local memory): each role copies only what it uses
   const int M = gar.M, N = gar.N, K = gar.K, kband = gar.kband;
   const bool lower = gar.lower;
   __syncthreads();
   if (M <= 0 || N <= 0 || K <= 0) return;
   if (threadIdx.x == 0) {
-    for (int st = 0; st < NST; ++st) {
+    for (int st = 0; st < C3_STAGES; ++st) {
       mbar_init(&gs->full[st], 1);
       mbar_init(&gs->empty[st], NCW);
     }
-    mbar_init(&gs->cfull, 1);
-    mbar_init(&gs->cempty, NCW);
     fence_barrier_init();
   }
   __syncthreads();
   const int tiles_m = cdiv(M, BM), tiles_n = cdiv(N, C3_BN);
-  const int nkc = cdiv(K, BKX);
+  const int nkc = cdiv(K, BK);
   int ntiles = 0;
   for (int tm = 0; tm < tiles_m; ++tm) ntiles += c3_tiles_in_row(tm, tiles_n, lower);
   const int warp = warp_id(), lane = lane_id();
-  double *Cs = reinterpret_cast<double *>(smem_al + NST * CF::STAGE_BYTES);  // [2][BM][CS_LD] (sub)
 
   if (warp == NCW) {
     // ============================ producer warp ============================
@@ -98,47 +83,34 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
         tn = 0;
         rowcnt = c3_tiles_in_row(++tm, tiles_n, lower);
       }
-      if (SUB) {
-        // this tile's C planes into the staging buffer once the consumers have read the previous one
-        if (tile > 0) mbar_wait(&gs->cempty, (tile - 1) & 1);
-        const int rows = min(BM, M - tm * BM), cols = min(C3_BN, N - tn * C3_BN);
-        const uint32_t rb = round16(cols * 8);
-        if (lane == 0) mbar_arrive_expect_tx(&gs->cfull, 2 * rb * rows);
-        __syncwarp();
-        const int64_t off = static_cast<int64_t>(tm * BM) * gar.ldc + tn * C3_BN;
-        RMX_CHECK(!gar.cr_end || (gar.Cr + off + (rows - 1) * gar.ldc + cols <= gar.cr_end &&
-                                  gar.Ci + off + (rows - 1) * gar.ldc + cols <= gar.ci_end));
-        bulk_rows(Cs, CF::CS_LD, gar.Cr + off, gar.ldc, rows, rb, &gs->cfull);
-        bulk_rows(Cs + CF::CS_PLANE, CF::CS_LD, gar.Ci + off, gar.ldc, rows, rb, &gs->cfull);
-      }
-      for (int kc = c3_kc_first(kband, tm, tn, BKX); kc < nkc; ++kc, ++it) {
-        const int st = it % NST, use = it / NST;
-        if (it >= NST) mbar_wait(&gs->empty[st], (use - 1) & 1);
+      for (int kc = c3_kc_first(kband, tm, tn); kc < nkc; ++kc, ++it) {
+        const int st = it % C3_STAGES, use = it / C3_STAGES;
+        if (it >= C3_STAGES) mbar_wait(&gs->empty[st], (use - 1) & 1);
         if (lane == 0) {
-          const int k0 = kc * BKX;
+          const int k0 = kc * BK;
           uint64_t *bar = &gs->full[st];
-          mbar_arrive_expect_tx(bar, CF::STAGE_BYTES);
-          const uint32_t s0 = smem_u32(smem_al + st * CF::STAGE_BYTES);
+          mbar_arrive_expect_tx(bar, C3_STAGE_BYTES);
+          const uint32_t s0 = smem_u32(smem_al + st * C3_STAGE_BYTES);
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
-            const uint32_t sa = s0 + p * CF::A_BYTES, sb = s0 + 2 * CF::A_BYTES + p * CF::B_BYTES;
+            const uint32_t sa = s0 + p * C3_A_BYTES, sb = s0 + 2 * C3_A_BYTES + p * C3_B_BYTES;
             if (A_KC) {
 #pragma unroll
-              for (int q = 0; q < BKX / 16; ++q)
+              for (int q = 0; q < 2; ++q)
                 tma_load_2d(sa + q * (BM * 128), tA[p], bar, ac0[p] + k0 + 16 * q, ar0[p] + tm * BM);
             } else {
 #pragma unroll
               for (int q = 0; q < BM / 16; ++q)
-                tma_load_2d(sa + q * (BKX * 128), tA[p], bar, ac0[p] + tm * BM + 16 * q, ar0[p] + k0);
+                tma_load_2d(sa + q * (BK * 128), tA[p], bar, ac0[p] + tm * BM + 16 * q, ar0[p] + k0);
             }
             if (B_KC) {
 #pragma unroll
-              for (int q = 0; q < BKX / 16; ++q)
+              for (int q = 0; q < 2; ++q)
                 tma_load_2d(sb + q * (C3_BN * 128), tB[p], bar, bc0[p] + k0 + 16 * q, br0[p] + tn * C3_BN);
             } else {
 #pragma unroll
               for (int q = 0; q < C3_BN / 16; ++q)
-                tma_load_2d(sb + q * (BKX * 128), tB[p], bar, bc0[p] + tn * C3_BN + 16 * q, br0[p] + k0);
+                tma_load_2d(sb + q * (BK * 128), tB[p], bar, bc0[p] + tn * C3_BN + 16 * q, br0[p] + k0);
             }
           }
         }
@@ -160,7 +132,7 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
         aoff[mi][1] = r * 128 + (((4 + t) ^ pg) << 4);
       } else {
         const int m = wm * WTM + mi * 8 + g, j2 = (m & 15) >> 1;
-        const uint32_t base = (m >> 4) * (BKX * 128) + ((m & 1) << 3);
+        const uint32_t base = (m >> 4) * (BK * 128) + ((m & 1) << 3);
         aoff[mi][0] = base + (2 * t) * 128 + ((j2 ^ (2 * t)) << 4);
         aoff[mi][1] = base + (2 * t + 1) * 128 + ((j2 ^ (2 * t + 1)) << 4);
       }
@@ -173,7 +145,7 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
         boff[ni][1] = r * 128 + (((4 + t) ^ pg) << 4);
       } else {
         const int n = wn * C3_WTN + ni * 8 + g, j2 = (n & 15) >> 1;
-        const uint32_t base = (n >> 4) * (BKX * 128) + ((n & 1) << 3);
+        const uint32_t base = (n >> 4) * (BK * 128) + ((n & 1) << 3);
         boff[ni][0] = base + (2 * t) * 128 + ((j2 ^ (2 * t)) << 4);
         boff[ni][1] = base + (2 * t + 1) * 128 + ((j2 ^ (2 * t + 1)) << 4);
       }
@@ -202,17 +174,17 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
           for (int h = 0; h < 2; ++h) t1[mi][ni][h] = t2[mi][ni][h] = t3[mi][ni][h] = 0.0;
       // lower mode: a warp tile entirely above the diagonal keeps only the ring protocol
       const bool upper_only = lower && (tm * BM + wm * WTM + WTM - 1 < tn * C3_BN + wn * C3_WTN);
-      for (int kc = c3_kc_first(kband, tm, tn, BKX); kc < nkc; ++kc, ++it) {
-        const int st = it % NST, use = it / NST;
+      for (int kc = c3_kc_first(kband, tm, tn); kc < nkc; ++kc, ++it) {
+        const int st = it % C3_STAGES, use = it / C3_STAGES;
         mbar_wait(&gs->full[st], use & 1);
         if (upper_only) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&gs->empty[st]);
           continue;
         }
-        const int krem = min(BKX, K - kc * BKX);
-        const uint32_t s0 = smem0 + st * CF::STAGE_BYTES;
-        const uint32_t sar = s0, sai = s0 + CF::A_BYTES, sbr = s0 + 2 * CF::A_BYTES, sbi = sbr + CF::B_BYTES;
+        const int krem = min(BK, K - kc * BK);
+        const uint32_t s0 = smem0 + st * C3_STAGE_BYTES;
+        const uint32_t sar = s0, sai = s0 + C3_A_BYTES, sbr = s0 + 2 * C3_A_BYTES, sbi = sbr + C3_B_BYTES;
         auto step = [&](const int k8, const bool partial) {
           double ar[MI][2], ai[MI][2], br[C3_NI][2], bi[C3_NI][2];
 #pragma unroll
@@ -274,9 +246,9 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
             }
           }
         };
-        if (krem == BKX) {
+        if (krem == BK) {
 #pragma unroll
-          for (int k8 = 0; k8 < BKX / 8; ++k8) step(k8, false);
+          for (int k8 = 0; k8 < BK / 8; ++k8) step(k8, false);
         } else {
 #pragma unroll 1
           for (int k8 = 0; k8 * 8 < krem; ++k8) step(k8, true);
@@ -284,9 +256,7 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
         __syncwarp();
         if (lane == 0) mbar_arrive(&gs->empty[st]);
       }
-      // epilogue: Re = T1 - T2, Im = (T3 - T1) - T2; straight to global memory (sub: C from the staging
-      // buffer, released afterwards)
-      if (SUB) mbar_wait(&gs->cfull, tile & 1);
+      // epilogue: Re = T1 - T2, Im = (T3 - T1) - T2; straight to global memory
       if (!upper_only) {
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
@@ -304,11 +274,7 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
               if (c >= N) continue;
               const double re = t1[mi][ni][h] - t2[mi][ni][h];
               const double im = (t3[mi][ni][h] - t1[mi][ni][h]) - t2[mi][ni][h];
-              if (SUB) {
-                const int cs = (wm * WTM + mi * 8 + arow) * CF::CS_LD + (c - tn * C3_BN);
-                crr[c] = Cs[cs] - re;
-                cri[c] = Cs[CF::CS_PLANE + cs] - im;
-              } else if (sub) {
+              if (sub) {
                 crr[c] -= re;
                 cri[c] -= im;
               } else {
@@ -317,10 +283,6 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
               }
             }
         }
-      }
-      if (SUB) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&gs->cempty);
       }
       ++tn;
     }
@@ -337,18 +299,16 @@ __device__ __forceinline__ void cgemm3(int M, int N, int K, const Op &ar, const 
   CGemmArgs g{ar, ai, br, bi, cr.at(r0, c0), ci.at(r0, c0), cr.ld, cr.end(), ci.end(), M, N, K, lower,
               sub, kband, alpha};
   uint8_t *s = gemm_smem_align(smem);
-  if (sub && ar.kc && br.kc) {
-    cgemm3_impl<true, true, true>(g, s, gs);
-  } else if (ar.kc) {
+  if (ar.kc) {
     if (br.kc)
-      cgemm3_impl<true, true, false>(g, s, gs);
+      cgemm3_impl<true, true>(g, s, gs);
     else
-      cgemm3_impl<true, false, false>(g, s, gs);
+      cgemm3_impl<true, false>(g, s, gs);
   } else {
     if (br.kc)
-      cgemm3_impl<false, true, false>(g, s, gs);
+      cgemm3_impl<false, true>(g, s, gs);
     else
-      cgemm3_impl<false, false, false>(g, s, gs);
+      cgemm3_impl<false, false>(g, s, gs);
   }
 }
 

@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(NT, 1)
   double *dr = slot + L.d_off, *di = dr + n, *vv = di + n;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
-  // complex products by the 3M single pass (cta_cgemm.cuh); RMX_TEPI_4M: the 4-product two-pass
-  // form (gemm_impl, nseg = 2) everywhere (A/B switch)
+  // complex products: 3M single pass (cta_cgemm.cuh, default) or the 4-product two-pass form
+  // (RMX_TEPI_4M, an A/B switch)
   auto cg = [&](int M, int N, int K, const Op &are, const Op &aim, const Op &bre, const Op &bim,
                 const MatView &cr, const MatView &ci, int r0, int c0, bool lower, bool sub, double alpha,
                 int kband) {
