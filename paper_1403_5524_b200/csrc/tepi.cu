@@ -224,12 +224,15 @@ __global__ void __launch_bounds__(NT, 1)
   double *dr = slot + L.d_off, *di = dr + n, *vv = di + n;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
-  // complex products: 3M single pass (cta_cgemm.cuh, default) or the 4-product two-pass form
-  // (RMX_TEPI_4M, an A/B switch)
+  // complex products: the products that write C (C = alpha A.B) by the 3M single pass
+  // (cta_cgemm.cuh); the trailing updates C -= A.B (K = 128 per tile, C read and written per tile) by
+  // the 4-product two-pass form of gemm_impl, whose 128 x 64 C tiles are staged through shared memory
+  // one tile ahead (3M measured +40 % there with C read in its epilogue, +33 % with staged C).
+  // RMX_TEPI_4M: the 4-product form everywhere (A/B switch).
   auto cg = [&](int M, int N, int K, const Op &are, const Op &aim, const Op &bre, const Op &bim,
                 const MatView &cr, const MatView &ci, int r0, int c0, bool lower, bool sub, double alpha,
                 int kband) {
-    if (c4m)
+    if (c4m || sub)
       cgemm(M, N, K, are, aim, bre, bim, cr, ci, r0, c0, lower, sub, alpha, kband, smg, gs);
     else
       cgemm3(M, N, K, are, aim, bre, bim, cr, ci, r0, c0, lower, sub, alpha, kband, smg, gs);
