@@ -9,7 +9,9 @@
 // through shared memory from coalesced row loads;
 // ascending k per output (deterministic). Pole guard as in R formation: |E - E_k| < 1e-10 gives
 // status RMX_E_POLE and NaN amplitudes. 2 nch nlev flops per energy - 1/(nch+1) of R formation, so
-// the kernel is a small fraction of the sweep; its bound is FP64 FMA issue.
+// the kernel is a small fraction of the sweep; its bound is FP64 FMA issue. As in R formation
+// (reading N1), the term of the pole nearest to E_e is left out of the contraction and added last
+// (dipole_g_pole_kernel, after the split-K partial planes are summed).
 //
 // Steps (10)-(12) (v = (1/2) U'^T g, M = (I - iK_oo)^{-1} v, sigma) run inside the T epilogue
 // (tepi.cu), which already holds (I - iK_oo)^{-1}.
@@ -33,11 +35,14 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
   extern __shared__ __align__(16) double dg_smem[];
   double(*Wt)[DG_LDW] = reinterpret_cast<double(*)[DG_LDW]>(dg_smem);                  // [k][channel]
   double(*Cs)[DG_BE] = reinterpret_cast<double(*)[DG_BE]>(dg_smem + DG_BK * DG_LDW);  // d_k/(E_k - E_e)
-  __shared__ int pole[DG_BE];
+  __shared__ int pole[DG_BE], kst[DG_BE];
   const int i0 = blockIdx.x * DG_BI;
   const int64_t e0 = static_cast<int64_t>(blockIdx.y) * DG_BE;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // energies tx*4.., channels ty*8..
-  if (threadIdx.x < DG_BE) pole[threadIdx.x] = 0;
+  if (threadIdx.x < DG_BE) {
+    pole[threadIdx.x] = 0;
+    kst[threadIdx.x] = (e0 + threadIdx.x < ne) ? nearest_pole(Ek, nlev, E[e0 + threadIdx.x]) : -1;
+  }
   double acc[DG_RI][DG_RE];
 #pragma unroll
   for (int r = 0; r < DG_RI; ++r)
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
       if (k < kend && e < ne) {
         const double diff = Ek[k] - E[e];
         if (fabs(diff) < kPoleGuard) pole[c] = 1;
-        v = d[k] / diff;
+        v = (k == kst[c]) ? 0.0 : d[k] / diff;  // nearest pole: added last (dipole_g_pole_kernel)
       }
       Cs[kk][c] = v;
     }
@@ -94,6 +99,19 @@ __global__ void __launch_bounds__(DG_NT, 2) dipole_g_kernel(const double *__rest
       if (i < nch) g[e * nch + i] = pl ? nan : acc[r][c];
     }
   }
+}
+
+// g += w_ik* d_k* / (E_k* - E_e), k* the pole nearest to E_e (reading N1: the large term last)
+__global__ void dipole_g_pole_kernel(const double *__restrict__ w, int64_t ldw, const double *__restrict__ Ek,
+                                     const double *__restrict__ d, const double *__restrict__ E, int nch,
+                                     int nlev, int64_t ne, double *__restrict__ g) {
+  const int64_t e = blockIdx.x;
+  if (e >= ne) return;
+  __shared__ int ks;
+  if (threadIdx.x == 0) ks = nearest_pole(Ek, nlev, E[e]);
+  __syncthreads();
+  const double c = d[ks] / (Ek[ks] - E[e]);
+  for (int i = threadIdx.x; i < nch; i += blockDim.x) g[e * nch + i] += w[static_cast<int64_t>(i) * ldw + ks] * c;
 }
 
 // g = sum of the nsplit partial planes, in plane order (deterministic)
@@ -141,6 +159,10 @@ cudaError_t launch_dipole_g(const double *w, int64_t ldw, const double *Ek, cons
       ce = cudaGetLastError();
       if (ce != cudaSuccess) return ce;
     }
+    dipole_g_pole_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(w, ldw, Ek, d, E + e0, static_cast<int>(nch),
+                                                                 static_cast<int>(nlev), n, g + e0 * nch);
+    ce = cudaGetLastError();
+    if (ce != cudaSuccess) return ce;
   }
   return cudaSuccess;
 }

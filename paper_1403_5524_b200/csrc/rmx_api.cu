@@ -516,7 +516,7 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
     if (ph) {
       // NEXT-1: g for this batch, then the amplitudes inside the T epilogue
       double *gb = static_cast<double *>(c->dg.p);
-      e = timed(c, RMX_KID_OTHER, 1, [&] {
+      e = timed(c, RMX_KID_OTHER, 3, [&] {
         return launch_dipole_g(w, ldw, Ek, ph->d, nch, nlev, E + b0, nb, gb, stb,
                                static_cast<double *>(c->dgpart.p),
                                static_cast<int64_t>(c->dgpart.bytes / sizeof(double)), c->stream);
@@ -582,7 +582,7 @@ rmx_rc rmx_dipole_amplitude(rmx_ctx *c, const double *w, int64_t ldw, const doub
   const int64_t ne1 = std::min<int64_t>(ne, static_cast<int64_t>(65535) * 64);
   rmx_rc rc = grow(c, c->dgpart, sizeof(double) * dipole_g_splits(nch, nlev, ne1) * ne1 * nch);
   if (rc != RMX_OK) return rc;
-  cudaError_t e = timed(c, RMX_KID_OTHER, 2, [&] {
+  cudaError_t e = timed(c, RMX_KID_OTHER, 3, [&] {  // contraction, split-K reduction, nearest-pole term
     return launch_dipole_g(w, ldw, Ek, d, nch, nlev, E, ne, g, status,
                            static_cast<double *>(c->dgpart.p),
                            static_cast<int64_t>(c->dgpart.bytes / sizeof(double)), c->stream);
