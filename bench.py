@@ -355,10 +355,10 @@ def main():
     ms_r, n_r = stats["rform"]
     fr, fk, ft = 0.0, 0.0, 0.0
     for s in range(args.warmup, nsteps):
-        a, b, c = flops_per_energy(nch, nlev, step_inputs[s]["no_host"])
-        fr += float(np.sum(np.broadcast_to(a, step_inputs[s]["no_host"].shape)))
-        fk += float(np.sum(b))
-        ft += float(np.sum(c))
+        f_r, f_k, f_t = flops_per_energy(nch, nlev, step_inputs[s]["no_host"])
+        fr += float(np.sum(np.broadcast_to(f_r, step_inputs[s]["no_host"].shape)))
+        fk += float(np.sum(f_k))
+        ft += float(np.sum(f_t))
     achieved_r = fr / (ms_r / 1e3) / 1e12 if ms_r > 0 else None
     # ---- the per-energy dense LA kernels (matching, T epilogue): executed algorithmic flops of the
     # routes in DESIGN.md §5.2/§5.3 (truncated back substitution; S^-1 route), the SURVEY §8(d) counts
@@ -407,12 +407,12 @@ def main():
             d = step_inputs[s]
             hs = {}
             for k in ("E", "F", "G", "Fp", "Gp"):
-                a = rmx.pinned_empty(tuple(d[k].shape))
-                a[:] = d[k].cpu().numpy()
-                hs[k] = a
-            a = rmx.pinned_empty(tuple(d["no"].shape), np.int32)
-            a[:] = d["no_host"]
-            hs["no"] = a
+                buf = rmx.pinned_empty(tuple(d[k].shape))
+                buf[:] = d[k].cpu().numpy()
+                hs[k] = buf
+            buf = rmx.pinned_empty(tuple(d["no"].shape), np.int32)
+            buf[:] = d["no_host"]
+            hs["no"] = buf
             hs["rowsum"] = rmx.pinned_empty((d["hi"] - d["lo"], nch))
             hs["status"] = rmx.pinned_empty((d["hi"] - d["lo"],), np.int32)
             host_steps.append(hs)

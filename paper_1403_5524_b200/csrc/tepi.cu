@@ -13,11 +13,11 @@
 // two real planes (re, im) and every complex product is two real DMMA GEMMs whose k range covers
 // both halves (GemmArgs::nseg = 2):
 //   0. Ar = I, Ai = -K_oo
-//   1. blocked right-looking LDL^T, outer blocks of 128 made of two 64-wide sub-blocks: each 64 x 64
+//   1. blocked right-looking LDL^T, outer blocks of 256 made of 64-wide sub-blocks: each 64 x 64
 //      diagonal block is factored in shared memory together with the inverse of its unit-lower
 //      factor, Tinv_b = L_bb^{-1} (written over the block, D to a vector); W21 = A21 Tinv_b^T
-//      (= L21 D_b), L21 = W21 D_b^{-1}; the second sub-block's columns are updated inside the panel,
-//      and the trailing matrix once per 128 columns, A22 -= W21 L21^T (lower tiles, K = 128)
+//      (= L21 D_b), L21 = W21 D_b^{-1}; the outer block's later columns are updated inside the
+//      panel, and the trailing matrix once per 256 columns, A22 -= W21 L21^T (lower tiles, K = 256)
 //   2. Z = L^{-1} in place, 128-row block rows: the 128 x 128 diagonal inverse from the two 64
 //      inverses, Z_{B,0:B} = -Tinv_B (L_{B,0:B} Z_{0:B,0:B})
 //   3. Y = D^{-1} Z
@@ -286,41 +286,37 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       TPH_MARK(0);  // copy (+ photo v)
-      // 1. blocked LDL^T, outer blocks of 128 = two 64-wide sub-blocks (diagonal factor + inverse in
-      // shared memory each); the trailing update runs once per 128 columns (K = 2 x 128 per C pass)
-      for (int P0 = 0; P0 < o; P0 += 2 * CB) {
-        const int W = min(2 * CB, o - P0), W1 = min(CB, W), W2 = W - W1, mb = o - P0 - W1, m = o - P0 - W;
-        // Y scratch row q <-> global row P0 + W1 + q; columns [0, W1) sub-block 1, [W1, W) sub-block 2
-        diag_ldlt_inv(Arv, Aiv, P0, W1, dr, di, sm.tri);
-        TPH_MARK(1);  // diagonal blocks
-        if (mb > 0) {
-          // W21 = A21 T1^T (= L21 D1) for all rows below sub-block 1
-          cg(mb, W1, W1, opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0), opk(Arv, P0, P0), opk(Aiv, P0, P0),
-             Yrv, Yiv, 0, 0, false, false, 1.0, 0);
+      // 1. blocked LDL^T, outer blocks of OB = 256 columns made of 64-wide sub-blocks (diagonal factor
+      // + inverse in shared memory each; W21, L21 and the update of the block's remaining columns
+      // per sub-block); the trailing matrix is updated once per outer block (K = OB per product)
+      constexpr int OB = 4 * CB;
+      for (int P0 = 0; P0 < o; P0 += OB) {
+        const int W = min(OB, o - P0), m = o - P0 - W;
+        // Y scratch row q <-> global row P0 + CB + q; column range of sub-block s: [s*CB, s*CB + ws)
+        for (int S = P0; S < P0 + W; S += CB) {
+          const int ws = min(CB, P0 + W - S), mb = o - S - ws, yr = S + ws - (P0 + CB), yc = S - P0;
+          const int rest = P0 + W - S - ws;  // columns of the outer block right of this sub-block
+          diag_ldlt_inv(Arv, Aiv, S, ws, dr, di, sm.tri);
+          TPH_MARK(1);  // diagonal blocks
+          if (mb == 0) break;
+          // W21 = A21 Tinv^T (= L21 D) for all rows below the sub-block
+          cg(mb, ws, ws, opk(Arv, S + ws, S), opk(Aiv, S + ws, S), opk(Arv, S, S), opk(Aiv, S, S), Yrv, Yiv,
+             yr, yc, false, false, 1.0, 0);
           TPH_MARK(2);  // W21 = A21 Tinv^T
-          scale_cols(Yrv, Yiv, 0, 0, Arv, Aiv, P0 + W1, P0, mb, W1, dr + P0, di + P0, sm.tri);
+          scale_cols(Yrv, Yiv, yr, yc, Arv, Aiv, S + ws, S, mb, ws, dr + S, di + S, sm.tri);
           TPH_MARK(3);  // L21 scaling
-          if (W2 > 0) {
-            // sub-block 2's columns: A[P0+W1:, P0+W1:P0+W] -= W21 L21[0:W2]^T
-            cg(mb, W2, W1, opk(Yrv, 0, 0), opk(Yiv, 0, 0), opk(Arv, P0 + W1, P0), opk(Aiv, P0 + W1, P0),
-               Arv, Aiv, P0 + W1, P0 + W1, false, true, 1.0, 0);
+          if (rest > 0) {
+            // the outer block's remaining columns: A[S+ws:, S+ws:P0+W] -= W21 L21[0:rest]^T
+            cg(mb, rest, ws, opk(Yrv, yr, yc), opk(Yiv, yr, yc), opk(Arv, S + ws, S), opk(Aiv, S + ws, S), Arv,
+               Aiv, S + ws, S + ws, false, true, 1.0, 0);
             TPH_MARK(4);
-            diag_ldlt_inv(Arv, Aiv, P0 + W1, W2, dr, di, sm.tri);
-            TPH_MARK(1);
-            if (m > 0) {
-              cg(m, W2, W2, opk(Arv, P0 + W, P0 + W1), opk(Aiv, P0 + W, P0 + W1), opk(Arv, P0 + W1, P0 + W1),
-                 opk(Aiv, P0 + W1, P0 + W1), Yrv, Yiv, W2, W1, false, false, 1.0, 0);
-              TPH_MARK(2);
-              scale_cols(Yrv, Yiv, W2, W1, Arv, Aiv, P0 + W, P0 + W1, m, W2, dr + P0 + W1, di + P0 + W1, sm.tri);
-              TPH_MARK(3);
-            }
           }
-          if (m > 0) {
-            // A22 -= [W21 W22] [L21 L22]^T (lower tiles), K = W per product
-            cg(m, m, W, opk(Yrv, W2, 0), opk(Yiv, W2, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0),
-               Arv, Aiv, P0 + W, P0 + W, true, true, 1.0, 0);
-            TPH_MARK(4);  // trailing updates
-          }
+        }
+        if (m > 0) {
+          // A22 -= [W21 ...] [L21 ...]^T over the whole outer block (lower tiles), K = W per product
+          cg(m, m, W, opk(Yrv, W - CB, 0), opk(Yiv, W - CB, 0), opk(Arv, P0 + W, P0), opk(Aiv, P0 + W, P0), Arv,
+             Aiv, P0 + W, P0 + W, true, true, 1.0, 0);
+          TPH_MARK(4);  // trailing updates
         }
       }
       // 2. Z = L^{-1} in place, 128-row block rows
