@@ -137,3 +137,23 @@ def test_gloo_world2_broadcast_case_and_partial_gather():
         expect = np.zeros((len(E), 2))
         expect[covered, 0], expect[covered, 1] = E[covered], -E[covered]
         assert np.array_equal(full, expect), rank
+
+
+def test_bench_gpus_refuses_without_enough_devices():
+    """`python bench.py --gpus N` outside torchrun launches N ranks through torch.distributed.run, and
+    refuses with one clear line (exit 2) when fewer than N GPUs are visible."""
+    import subprocess
+    import sys
+    if torch.cuda.is_available() and torch.cuda.device_count() >= 64:
+        pytest.skip("box has 64 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "64", "--steps", "1"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 2, out.stdout + out.stderr
+    assert "refusing to run 64 ranks" in out.stderr
+    # launched with a WORLD_SIZE that disagrees with --gpus: refused as well
+    env.update(WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--steps", "1"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 2 and "WORLD_SIZE=2" in out.stderr, out.stdout + out.stderr
