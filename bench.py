@@ -361,13 +361,15 @@ def main():
         ft += float(np.sum(f_t))
     achieved_r = fr / (ms_r / 1e3) / 1e12 if ms_r > 0 else None
     # ---- the per-energy dense LA kernels (matching, T epilogue): executed algorithmic flops of the
-    # routes in DESIGN.md §5.2/§5.3 (truncated back substitution; S^-1 route), the SURVEY §8(d) counts
+    # routes in DESIGN.md §5.2/§5.3 (truncated back substitution; complex LDL^T inverse of I - iK_oo:
+    # LDL^T 4/3 o^3 with 4-product complex updates, L^-1 and Z^T D^-1 Z o^3 each with 3M), the
+    # SURVEY §8(d) counts
     # beside them, FP64 DMMA fraction, and HBM GB/s from the committed ncu capture's bytes per launch
     fk_x, ft_x = 0.0, 0.0
     for s in range(args.warmup, nsteps):
         no = step_inputs[s]["no_host"].astype(np.float64)
         fk_x += float(np.sum((2.0 / 3.0) * nch ** 3 + nch ** 2 * no + no ** 3))
-        ft_x += float(np.sum(3.0 * no ** 3))
+        ft_x += float(np.sum((10.0 / 3.0) * no ** 3))
     la = {}
     for kname, key, fx, fs in (("match_kernel", "match", fk_x, fk), ("tepi_kernel", "tepi", ft_x, ft)):
         ms_k, n_k = stats.get(key, (0.0, 0))

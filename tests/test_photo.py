@@ -143,3 +143,25 @@ def test_gpu_photo(ctx, nch, nlev, eps_hi):
         assert nrel(fused["mabs2"][e].cpu().numpy(), ref["mabs2"][e]) < TOL_M, e
     assert nrel(sig, ref["sigma"]) < TOL_M
     assert nrel(fused["sigma"].cpu().numpy(), ref["sigma"]) < TOL_M
+
+
+@pytest.mark.gpu
+def test_gpu_photo_near_poles(ctx):
+    """NEXT-1 at energies 1e-5 and 1e-3 from poles (the nearest pole's term of g is summed apart and
+    added last, reading N1, as in R formation): g, |M_j|^2 and sigma against the oracle."""
+    import torch
+    c, Ek, w, d, _ = _case_with_dipole(150, 517, seed=77, ne=4, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
+    inside = Ek[(Ek > 1.0) & (Ek < 8.5)]
+    E = np.sort(np.concatenate([p + np.array([-1e-5, 1e-5, 1e-3]) for p in inside[[5, len(inside) // 2]]]))
+    F, G, Fp, Gp = syn.asymptotic(c.eps, E, c.a)
+    no = syn.n_open(c.eps, E)
+    ref = oracle.photo_sweep(w, Ek, d, c.a, E, F, G, Fp, Gp, no, E0=-2.0)
+    g, st = ctx.dipole_amplitude(w, Ek, d, E)
+    fused = ctx.sweep_photo(w, Ek, d, c.a, E, F, G, Fp, Gp, no, -2.0, want_mabs2=True)
+    torch.cuda.synchronize()
+    g = g.cpu().numpy()
+    assert int((st != 0).sum()) == 0 and int((fused["status"] != 0).sum()) == 0
+    for e in range(len(E)):
+        assert nrel(g[e], ref["g"][e]) < 1e-12, (E[e], nrel(g[e], ref["g"][e]))
+        assert nrel(fused["mabs2"][e].cpu().numpy(), ref["mabs2"][e]) < TOL_M, e
+    assert nrel(fused["sigma"].cpu().numpy(), ref["sigma"]) < TOL_M
