@@ -21,7 +21,10 @@ ARGS1="--steps 1 --warmup 3 --no-e2e --no-cpu-baseline --repeats 1"
 ncu --set full --import-source on --clock-control none -k regex:"oz_gemm2|oz_convert_kernel" -s 40 -c 2 \
     -o gpurun_out/${TAG}_int8_full python bench.py $ARGS1 > gpurun_out/ncu_pi8.log 2>&1
 echo "ncu int8 rc=$?"
-ncu --set full --import-source on --clock-control none -k regex:"match_kernel|tepi_kernel" -s 6 -c 2 \
-    -o gpurun_out/${TAG}_la_full python bench.py $ARGS1 > gpurun_out/ncu_la.log 2>&1
-echo "ncu la rc=$?"
+ncu --set full --import-source on --clock-control none -k regex:tepi_kernel -s 3 -c 1 \
+    -o gpurun_out/${TAG}_tepi_full python bench.py $ARGS1 > gpurun_out/ncu_tepi.log 2>&1
+echo "ncu tepi rc=$?"
+ncu --set full --import-source on --clock-control none -k regex:match_kernel -s 3 -c 1 \
+    -o gpurun_out/${TAG}_match_full python bench.py $ARGS1 > gpurun_out/ncu_match.log 2>&1
+echo "ncu match rc=$?"
 tail -c 400 gpurun_out/${TAG}_bench_default.json
