@@ -258,10 +258,15 @@ def main():
     my_blocks = rdist.cyclic_blocks(ne, batch, world, rank)
     nsteps = args.warmup + args.steps
 
-    # Steps walk this rank's blocks spread evenly over the whole mesh (not just its first blocks),
-    # so a short run sees the same mix of open-channel counts n_o(E) as the full sweep.
+    # The K timed steps walk this rank's blocks spread evenly over the whole mesh (timed step t takes
+    # the block at quantile (t + 0.5)/K), so a short run sees the same mix of open-channel counts
+    # n_o(E) - and so of matching / T cost - as the full sweep; warm-up step w repeats timed block
+    # w mod K (warm-up must not take blocks out of the timed mix).
+    def timed_block(blocks, t):
+        return blocks[min(len(blocks) - 1, int((t + 0.5) * len(blocks) / args.steps))]
+
     def block_of_step(s):
-        return my_blocks[min(len(my_blocks) - 1, int((s + 0.5) * len(my_blocks) / nsteps))]
+        return timed_block(my_blocks, (s % args.steps) if s < args.warmup else s - args.warmup)
 
     step_inputs = []
     for s in range(nsteps):
@@ -285,8 +290,7 @@ def main():
         out = []
         for r in range(world):
             blocks = rdist.cyclic_blocks(ne, batch, world, r)
-            idx = [np.arange(*rdist.block_range(blocks[min(len(blocks) - 1, int((s + 0.5) * len(blocks) / nsteps))],
-                                                ne, batch)) for s in range(args.warmup, nsteps)]
+            idx = [np.arange(*rdist.block_range(timed_block(blocks, t), ne, batch)) for t in range(args.steps)]
             out.append(np.concatenate(idx))
         return out
     shards = timed_shards() if world > 1 else None
