@@ -33,10 +33,6 @@ struct CGemmArgs {
   bool lower, sub;  // sub: C -= A.B; else C = alpha A.B
   int kband;        // as GemmArgs::kband
   double alpha;
-  // optional second output (set mode): C2 = (alpha A.B) diag(d)^{-1} with the complex d_j of output
-  // column j (the LDL^T panel's L21 = W21 D^{-1} next to W21), same pitch as C
-  double *C2r = nullptr, *C2i = nullptr;
-  const double *dr = nullptr, *di = nullptr;
 };
 
 __device__ __forceinline__ int c3_tiles_in_row(int tm, int tiles_n, bool lower) {
@@ -160,8 +156,6 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
     const int64_t ldc = gar.ldc;
     const bool sub = gar.sub;
     const double alpha = gar.alpha;
-    double *const C2r = gar.C2r, *const C2i = gar.C2i;
-    const double *const dre = gar.dr, *const dim = gar.di;
 #ifdef RMX_CHECKS
     const double *cr_end = gar.cr_end, *ci_end = gar.ci_end;
 #endif
@@ -284,15 +278,8 @@ static __device__ __noinline__ void cgemm3_impl(const CGemmArgs &gar, uint8_t *s
                 crr[c] -= re;
                 cri[c] -= im;
               } else {
-                const double vr = alpha * re, vi = alpha * im;
-                crr[c] = vr;
-                cri[c] = vi;
-                if (C2r) {
-                  const double a = dre[c], b = dim[c], den = fma(a, a, b * b);
-                  const double ir = a / den, ii = -b / den;
-                  C2r[static_cast<int64_t>(r) * ldc + c] = vr * ir - vi * ii;
-                  C2i[static_cast<int64_t>(r) * ldc + c] = fma(vr, ii, vi * ir);
-                }
+                crr[c] = alpha * re;
+                cri[c] = alpha * im;
               }
             }
         }

@@ -299,23 +299,12 @@ __global__ void __launch_bounds__(NT, 1)
           diag_ldlt_inv(Arv, Aiv, S, ws, dr, di, sm.tri);
           TPH_MARK(1);  // diagonal blocks
           if (mb == 0) break;
-          // W21 = A21 Tinv^T (= L21 D) for all rows below the sub-block, and L21 = W21 D^{-1} over A21
-          if (c4m) {
-            cg(mb, ws, ws, opk(Arv, S + ws, S), opk(Aiv, S + ws, S), opk(Arv, S, S), opk(Aiv, S, S), Yrv, Yiv,
-               yr, yc, false, false, 1.0, 0);
-            scale_cols(Yrv, Yiv, yr, yc, Arv, Aiv, S + ws, S, mb, ws, dr + S, di + S, sm.tri);
-          } else {
-            // one 3M pass writing both (the L21 scaling in its epilogue)
-            CGemmArgs g{opk(Arv, S + ws, S), opk(Aiv, S + ws, S), opk(Arv, S, S), opk(Aiv, S, S),
-                        Yrv.at(yr, yc), Yiv.at(yr, yc), ldo, Yrv.end(), Yiv.end(), mb, ws, ws, false, false, 0,
-                        1.0};
-            g.C2r = Arv.at(S + ws, S);
-            g.C2i = Aiv.at(S + ws, S);
-            g.dr = dr + S;
-            g.di = di + S;
-            cgemm3_impl<true, true>(g, gemm_smem_align(smg), gs);
-          }
-          TPH_MARK(2);  // W21 = A21 Tinv^T (+ L21)
+          // W21 = A21 Tinv^T (= L21 D) for all rows below the sub-block
+          cg(mb, ws, ws, opk(Arv, S + ws, S), opk(Aiv, S + ws, S), opk(Arv, S, S), opk(Aiv, S, S), Yrv, Yiv,
+             yr, yc, false, false, 1.0, 0);
+          TPH_MARK(2);  // W21 = A21 Tinv^T
+          scale_cols(Yrv, Yiv, yr, yc, Arv, Aiv, S + ws, S, mb, ws, dr + S, di + S, sm.tri);
+          TPH_MARK(3);  // L21 scaling
           if (rest > 0) {
             // the outer block's remaining columns: A[S+ws:, S+ws:P0+W] -= W21 L21[0:rest]^T
             cg(mb, rest, ws, opk(Yrv, yr, yc), opk(Yiv, yr, yc), opk(Arv, S + ws, S), opk(Aiv, S + ws, S), Arv,

@@ -37,7 +37,7 @@ ours = {k: v for k, v in agg.items() if any(s in k for s in ("rform", "match_ker
                                                                 "dipole_g", "conv_gauss", "maxwell"))}
 tot_ours = sum(v[1] for v in ours.values()) or 1.0
 lines = [f"# Round {rnd} ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-         "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline` (darc, 296 energies/step, "
+         "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --repeats 1` (darc, 296 energies/step, "
          "INT8-CRT R formation).",
          "Per-launch times are cold-cache and serialised: compare shares, not absolutes.", "",
          "| kernel | launches | total ms | share of all | share of librmx |", "|---|---|---|---|---|"]
