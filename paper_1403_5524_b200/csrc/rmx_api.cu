@@ -2,6 +2,7 @@
 // the streaming sweep driver and launch instrumentation. All arithmetic of the method lives in
 // rform.cu / match.cu / tepi.cu; this file only validates, allocates and launches.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -290,7 +291,14 @@ static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double
       return launch_rform(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->stream, err);
     }
     if (!c->i8s.aux) {
-      cudaStreamCreateWithFlags(&c->i8s.aux, cudaStreamNonBlocking);
+      // the conversion stream gets the highest priority: the block scheduler then places conversion
+      // CTAs (no shared memory) next to the resident INT8 GEMM CTAs as soon as registers / threads
+      // free up, instead of after the GEMM grid's queued CTAs (RMX_I8_AUX_PRIO=0 restores the default
+      // priority - A/B switch)
+      int lo_prio = 0, hi_prio = 0;
+      cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+      static const bool aux_default = getenv("RMX_I8_AUX_PRIO") && getenv("RMX_I8_AUX_PRIO")[0] == '0';
+      cudaStreamCreateWithPriority(&c->i8s.aux, cudaStreamNonBlocking, aux_default ? lo_prio : hi_prio);
       for (cudaEvent_t *ev : {&c->i8s.start, &c->i8s.conv_done[0], &c->i8s.conv_done[1], &c->i8s.gemm_done[0],
                               &c->i8s.gemm_done[1]})
         cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
