@@ -291,14 +291,9 @@ static cudaError_t form_R(rmx_ctx *c, const double *w, int64_t ldw, const double
       return launch_rform(w, ldw, Ek, nch, nlev, a, E, ne, R, status, c->stream, err);
     }
     if (!c->i8s.aux) {
-      // the conversion stream gets the highest priority: the block scheduler then places conversion
-      // CTAs (no shared memory) next to the resident INT8 GEMM CTAs as soon as registers / threads
-      // free up, instead of after the GEMM grid's queued CTAs (RMX_I8_AUX_PRIO=0 restores the default
-      // priority - A/B switch)
-      int lo_prio = 0, hi_prio = 0;
-      cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-      static const bool aux_default = getenv("RMX_I8_AUX_PRIO") && getenv("RMX_I8_AUX_PRIO")[0] == '0';
-      cudaStreamCreateWithPriority(&c->i8s.aux, cudaStreamNonBlocking, aux_default ? lo_prio : hi_prio);
+      // default priority: a highest-priority conversion stream (to place conversion CTAs next to the
+      // resident GEMM CTAs) made the darc bench stall for > 20 min (round 2) - not used
+      cudaStreamCreateWithFlags(&c->i8s.aux, cudaStreamNonBlocking);
       for (cudaEvent_t *ev : {&c->i8s.start, &c->i8s.conv_done[0], &c->i8s.conv_done[1], &c->i8s.gemm_done[0],
                               &c->i8s.gemm_done[1]})
         cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
