@@ -147,13 +147,10 @@ __global__ void __launch_bounds__(256) oz_rowmax_kernel(const double *__restrict
 // The k range is split over gridDim.y CTAs whose partial maxima meet by atomicMax on the float bit
 // patterns (non-negative floats order like their bits; max is order-independent: deterministic).
 constexpr int XM_ROWS = 16, XM_KT = 512, XM_KSPLIT = 8;
-// No shared memory (the |d| values are read through L1 from the 8 x nlev table, L2-resident): with
-// its CTA needing no shared memory the kernel can run next to a resident INT8 GEMM CTA (which holds
-// ~225 of the SM's 228 KB) instead of waiting for the GEMM grid to drain, so the conversion pass of
-// the next chunk overlaps the current chunk's GEMM.
 __global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__ w, int64_t ldw, int nch, int nlev,
                                                       int ne, const double *__restrict__ dbuf,
                                                       float *__restrict__ xmax) {
+  __shared__ float ds[8][XM_KT];
   const int r0 = blockIdx.x * XM_ROWS + warp_id() * 2;
   float mx[2][8];
 #pragma unroll
@@ -164,6 +161,14 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__
   const int t0 = static_cast<int>((static_cast<int64_t>(ntile) * blockIdx.y) / gridDim.y);
   const int t1 = static_cast<int>((static_cast<int64_t>(ntile) * (blockIdx.y + 1)) / gridDim.y);
   for (int k0 = t0 * XM_KT; k0 < t1 * XM_KT; k0 += XM_KT) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < 8 * XM_KT; q += blockDim.x) {
+      const int e = q / XM_KT, kk = q % XM_KT;
+      ds[e][kk] = (e < ne && k0 + kk < nlev)
+                      ? __double2float_ru(fabs(dbuf[static_cast<int64_t>(e) * nlev + k0 + kk]))
+                      : 0.0f;
+    }
+    __syncthreads();
     // all 2 x 16 w loads of this lane issued before any use (the loop is latency-bound otherwise)
     float wv[2][XM_KT / 32];
 #pragma unroll
@@ -177,17 +182,13 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const double *__restrict__
       }
     }
 #pragma unroll
-    for (int q = 0; q < XM_KT / 32; ++q) {
-      const int k = k0 + lane_id() + 32 * q;
-      float dv[8];
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        dv[e] = (e < ne && k < nlev) ? __double2float_ru(fabs(__ldg(dbuf + static_cast<int64_t>(e) * nlev + k))) : 0.0f;
+      for (int q = 0; q < XM_KT / 32; ++q) {
+        const int kk = lane_id() + 32 * q;
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx[r][e] = fmaxf(mx[r][e], __fmul_ru(wv[r][q], dv[e]));
-    }
+        for (int e = 0; e < 8; ++e) mx[r][e] = fmaxf(mx[r][e], __fmul_ru(wv[r][q], ds[e][kk]));
+      }
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r)
