@@ -58,6 +58,7 @@ def ncu_traffic(workload: str, batch: int, kernel: str = "rform"):
         except (OSError, ValueError):
             continue
         tot, hit = 0.0, False
+        dur = 0.0
         for name, ent in d.items():
             if kernel not in name:
                 continue
@@ -65,8 +66,10 @@ def ncu_traffic(workload: str, batch: int, kernel: str = "rform"):
             rd, wr = ent.get("dram__bytes_read.bytes"), ent.get("dram__bytes_write.bytes")
             if wl.get("config") == workload and wl.get("energies_per_launch") == batch and rd and wr:
                 tot += rd + wr
+                dur += ent.get("gpu__time_duration.sum") or 0.0
                 hit = True
         if hit:
+            ncu_traffic.duration_ms = dur  # the captured launch's own (cold, serialised) duration
             return tot, os.path.basename(path)
     return None, None
 
@@ -380,12 +383,16 @@ def main():
         if ms_k <= 0:
             continue
         tb, tsrc = ncu_traffic(args.config, batch, kernel=kname)
+        # DRAM rate of the one launch ncu captured (its bytes over its own duration): the captured
+        # block's n_open differs from this run's mix, so its bytes are not divided by this run's time
+        tms = getattr(ncu_traffic, "duration_ms", 0.0) if tb else 0.0
         la[key] = {"ms": round(ms_k, 3), "launches": n_k,
                    "tflops_executed": fx / (ms_k / 1e3) / 1e12, "tflops_survey_count": fs / (ms_k / 1e3) / 1e12,
                    "frac_fp64_dmma_peak": fx / (ms_k / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
-                   "hbm_gbs": (tb * n_k / (ms_k / 1e3) / 1e9) if tb else None,
-                   "hbm_frac": (tb * n_k / (ms_k / 1e3) / 1e9 / float(measured_peaks().get("hbm_gbs", 6543.7)))
-                   if tb else None,
+                   "ncu_dram_bytes_per_launch": tb,
+                   "ncu_hbm_gbs": (tb / (tms / 1e3) / 1e9) if tb and tms else None,
+                   "ncu_hbm_frac": (tb / (tms / 1e3) / 1e9 / float(measured_peaks().get("hbm_gbs", 6543.7)))
+                   if tb and tms else None,
                    "traffic_source": tsrc}
     path_tflops = (fr + fk + ft) / (ms / 1e3) / 1e12
     ms_g, n_g = stats.get("i8gemm", (0.0, 0))
