@@ -91,6 +91,78 @@ __device__ __forceinline__ void mirror_lower(double *P, int64_t ld, int o, doubl
   __syncthreads();
 }
 
+// |T|^2 = 4 (Im^2 + (delta - Re)^2) and the row sums straight from the LOWER triangles of Re A^{-1} (P)
+// and Im A^{-1} (X), 32 x 32 tiles staged through shared memory (the mirror passes are not needed):
+// tile (bi, bj), bi >= bj, yields |T|^2 of its own elements and of the mirrored tile (bj, bi) (on a
+// diagonal tile the upper half is filled from the lower one: bitwise symmetric |T|^2), its row sums
+// go to part[bj][i] and its column sums to part[bi][j]; then rowsum_i = sum_q part[q][i] in q order
+// (fixed order: deterministic). part: nb x o scratch (pitch o). Returns the non-finite flag.
+__device__ __noinline__ int tiled_t2(const double *P, const double *X, int64_t ld, int o, int n, double *T2e,
+                                     double *rowsum, double *part, double *smem) {
+  constexpr int TL = 33;
+  const int nb = (o + 31) / 32, lane = lane_id();
+  double *tile = smem + warp_id() * 32 * TL;
+  int bad = 0;
+  __syncthreads();
+  for (int b = warp_id(); b < nb * (nb + 1) / 2; b += NW) {
+    int bi = 0, rem = b;
+    while (rem > bi) {
+      rem -= bi + 1;
+      ++bi;
+    }
+    const int bj = rem;
+    const bool diag = bi == bj;
+    for (int r = 0; r < 32; ++r) {
+      const int gi = bi * 32 + r, gj = bj * 32 + lane;
+      double v = 0.0;
+      if (gi < o && gj < o && (!diag || lane <= r)) {
+        const double x = X[static_cast<int64_t>(gi) * ld + gj];
+        const double pv = (gi == gj ? 1.0 : 0.0) - P[static_cast<int64_t>(gi) * ld + gj];
+        v = 4.0 * fma(x, x, pv * pv);
+      }
+      tile[r * TL + lane] = v;
+    }
+    __syncwarp();
+    if (diag)
+      for (int r = 0; r < 32; ++r)
+        if (lane > r) tile[r * TL + lane] = tile[lane * TL + r];  // upper half from the lower one
+    __syncwarp();
+    // row sums of the tile (lane = row) and of its mirror (lane = column)
+    double rs = 0.0, cs = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      rs += tile[lane * TL + q];
+      cs += tile[q * TL + lane];
+    }
+    if (!isfinite(rs)) bad = 1;
+    const int gi = bi * 32 + lane, gj = bj * 32 + lane;
+    if (gi < o) part[static_cast<int64_t>(bj) * o + gi] = rs;
+    if (!diag && gj < o) part[static_cast<int64_t>(bi) * o + gj] = cs;
+    if (T2e) {
+      for (int r = 0; r < 32; ++r) {
+        const int ri = bi * 32 + r, cj = bj * 32 + lane;
+        if (ri < o && cj < o) T2e[static_cast<int64_t>(ri) * n + cj] = tile[r * TL + lane];
+        const int rj = bj * 32 + r, ci = bi * 32 + lane;
+        if (!diag && rj < o && ci < o) T2e[static_cast<int64_t>(rj) * n + ci] = tile[lane * TL + r];
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double s = 0.0;
+    if (i < o)
+      for (int q = 0; q < nb; ++q) s += part[static_cast<int64_t>(q) * o + i];
+    if (rowsum) rowsum[i] = s;
+  }
+  if (T2e) {  // closed rows / columns: zero
+    for (int i = warp_id(); i < n; i += NW)
+      for (int j = lane; j < n; j += 32)
+        if (i >= o || j >= o) T2e[static_cast<int64_t>(i) * n + j] = 0.0;
+  }
+  return bad;
+}
+
 // LDL^T of the W x W (W <= 64) complex symmetric diagonal block A[p0.., p0..] (lower triangle of
 // the planes ar, ai) without pivoting, fused with the inverse of its unit-lower factor: in shared
 // memory row r holds X = L^{-1} in columns < c and the not yet eliminated part of A in columns
@@ -389,12 +461,18 @@ __global__ void __launch_bounds__(NT, 1)
                false, 1.0, 1, smg, gs);
       }
       TPH_MARK(6);  // Y = D^{-1} Z and A^{-1} = Z^T Y
-      // 5. symmetric A^{-1}: upper triangles from the lower ones
-      mirror_lower(Pv.base, ldo, o, sm.gemm);
-      mirror_lower(Yiv.base, ldo, o, sm.gemm);
+      // 5. symmetric A^{-1}: upper triangles from the lower ones - needed only by the NEXT-1 / NEXT-2
+      // options, which read whole rows; |T|^2 and the row sums come from the lower triangles alone
+      if (pa.g || lv.omega) {
+        mirror_lower(Pv.base, ldo, o, sm.gemm);
+        mirror_lower(Yiv.base, ldo, o, sm.gemm);
+      }
     }
+    const bool tiled = !(pa.g || lv.omega) && o > 0;
+    if (tiled)  // the Yr plane (free after step 4) holds the partial row sums
+      bad |= tiled_t2(Pv.base, Yiv.base, ldo, o, n, T2e, rowsum ? rowsum + e * n : nullptr, Yrv.base, sm.gemm);
     // epilogue: |T|^2 = 4 (Im^2 + (delta - Re)^2), row sums in fixed order
-    for (int i = warp_id(); i < n; i += NW) {
+    for (int i = warp_id(); i < (tiled ? 0 : n); i += NW) {
       double s = 0.0;
       const double *xr = Yiv.at(i, 0), *pr = Pv.at(i, 0);
       constexpr int U = 4;  // 2U independent loads in flight per lane
