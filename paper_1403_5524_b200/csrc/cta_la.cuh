@@ -472,11 +472,21 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
   int singular = 0;
   for (int s0 = 0; s0 < bw; s0 += SPW) {
     const int c0 = p0 + s0, w = min(SPW, bw - s0), nr = n - c0;
-    // 1. stage the sub-panel rows c0..n-1, columns c0..c0+w
+    // 1. stage the sub-panel rows c0..n-1, columns c0..c0+w (SU loads in flight per thread)
+    constexpr int SU = 8;
     __syncthreads();
-    for (int q = threadIdx.x; q < nr * SPW; q += NT) {
-      const int r = q / SPW, c = q % SPW;
-      sp[r * SP_LD + c] = c < w ? M[static_cast<int64_t>(c0 + r) * ld + c0 + c] : 0.0;
+    for (int q0 = threadIdx.x; q0 < nr * SPW; q0 += NT * SU) {
+      double v[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int q = q0 + u * NT, r = q / SPW, c = q % SPW;
+        v[u] = (q < nr * SPW && c < w) ? M[static_cast<int64_t>(c0 + r) * ld + c0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int q = q0 + u * NT;
+        if (q < nr * SPW) sp[(q / SPW) * SP_LD + q % SPW] = v[u];
+      }
     }
     __syncthreads();
     // 2. factor in shared memory

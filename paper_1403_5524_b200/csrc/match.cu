@@ -202,15 +202,27 @@ __global__ void __launch_bounds__(NT, 1)
       const int qi = (i < o) ? nc + i : i - o;  // solution row of channel i
       const double *Yi = Mw + static_cast<int64_t>(qi) * ldm + npad;
       double *Ki = Ke + static_cast<int64_t>(i) * ldk;
-      for (int j = lane_id(); j < ncolk; j += 32) {
-        double v;
-        if (j < o) {
-          v = -Yi[j];
-          if (i < o && !isfinite(v)) bad = 1;
-        } else {
-          v = (i == j) ? -1.0 : 0.0;
+      constexpr int U = 8;  // U independent loads in flight per lane
+      for (int j0 = lane_id(); j0 < ncolk; j0 += 32 * U) {
+        double y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + 32 * u;
+          y[u] = (j < o && j < ncolk) ? Yi[j] : 0.0;
         }
-        Ki[j] = v;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + 32 * u;
+          if (j >= ncolk) continue;
+          double v;
+          if (j < o) {
+            v = -y[u];
+            if (i < o && !isfinite(v)) bad = 1;
+          } else {
+            v = (i == j) ? -1.0 : 0.0;
+          }
+          Ki[j] = v;
+        }
       }
     }
     bad = __syncthreads_or(bad);

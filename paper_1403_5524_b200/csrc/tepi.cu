@@ -240,12 +240,23 @@ __device__ __forceinline__ void scale_cols(const MatView &sr, const MatView &si,
     idi[j] = -b / den;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < m * 64; q += NT) {
-    const int i = q >> 6, j = q & 63;
-    if (j < w) {
-      const double xr = *sr.at(sr0 + i, sc0 + j), xi = *si.at(sr0 + i, sc0 + j);
-      *tr.at(dr0 + i, dc0 + j) = xr * idr[j] - xi * idi[j];
-      *ti.at(dr0 + i, dc0 + j) = fma(xr, idi[j], xi * idr[j]);
+  constexpr int U = 8;  // 2U independent loads in flight per thread (the pass is latency-bound)
+  for (int q0 = threadIdx.x; q0 < m * 64; q0 += NT * U) {
+    double xr[U], xi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * NT, i = q >> 6, j = q & 63;
+      const bool ok = q < m * 64 && j < w;
+      xr[u] = ok ? *sr.at(sr0 + i, sc0 + j) : 0.0;
+      xi[u] = ok ? *si.at(sr0 + i, sc0 + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * NT, i = q >> 6, j = q & 63;
+      if (q < m * 64 && j < w) {
+        *tr.at(dr0 + i, dc0 + j) = xr[u] * idr[j] - xi[u] * idi[j];
+        *ti.at(dr0 + i, dc0 + j) = fma(xr[u], idi[j], xi[u] * idr[j]);
+      }
     }
   }
 }
