@@ -25,7 +25,6 @@ constexpr int WTM = BM / WM, WTN = BN / WN;  // 32 x 32 warp tile
 constexpr int MI = WTM / 8, NI = WTN / 8;    // 4 x 4 DMMA fragments
 constexpr int PB = 32;                        // inner panel / triangle width of the factorizations
 constexpr int NB = 4 * PB;                    // outer block width (K of the big trailing GEMMs)
-constexpr int PW = 2 * PB;                    // LU panel width (panel_lu: bw <= PW)
 constexpr int STAGES = 3;                     // A/B ring depth
 // TMA boxes are 16 doubles (128 B, the SWIZZLE_128B span) wide:
 //   view 0: {16, 128} rows   k-contiguous A slices (2 boxes per BK = 32)
@@ -457,7 +456,7 @@ __device__ __forceinline__ void block_argmax(double &v, int &idx, double *redv, 
   }
 }
 
-// LU with partial pivoting of the panel M[p0:n, p0:p0+bw] (bw <= PW = 64), in place: multipliers
+// LU with partial pivoting of the panel M[p0:n, p0:p0+bw] (bw <= 32), in place: multipliers
 // below the diagonal, U on and above; pivot rows (absolute) in ipiv[0..bw). Returns 1 on an exact
 // zero pivot. Pivot rule: max |a_ij| over the remaining rows, ties -> lowest row (the oracle's rule).
 // The panel is processed in sub-panels of SPW = 8 columns held in shared memory (sp: >= (n-p0)*9
@@ -577,33 +576,28 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
         }
 #pragma unroll
         for (int q = 0; q < SPW; ++q) {
-          ubuf[q * PW + threadIdx.x] = x[q];
+          ubuf[q * PB + threadIdx.x] = x[q];
           if (q < w) M[static_cast<int64_t>(c0 + q) * ld + c] = x[q];
         }
       }
       __syncthreads();
-      // rows c0+w..n-1: M[i][c] -= sum_q L[i][q] U[q][c]; warp per row, lane per column (32-column
-      // chunks)
+      // rows c0+w..n-1: M[i][c] -= sum_q L[i][q] U[q][c]; warp per row, lane per column
       constexpr int UNR = 8;
-      for (int c32 = 0; c32 < nc; c32 += 32) {
-        const int col = c32 + lane;
-        const bool okc = col < nc;
-        for (int r0 = w + warp; r0 < nr; r0 += NW * UNR) {
-          double x[UNR];
+      for (int r0 = w + warp; r0 < nr; r0 += NW * UNR) {
+        double x[UNR];
 #pragma unroll
-          for (int q = 0; q < UNR; ++q) {
-            const int r = r0 + q * NW;
-            x[q] = (r < nr && okc) ? M[static_cast<int64_t>(c0 + r) * ld + cr0 + col] : 0.0;
-          }
+        for (int q = 0; q < UNR; ++q) {
+          const int r = r0 + q * NW;
+          x[q] = (r < nr && lane < nc) ? M[static_cast<int64_t>(c0 + r) * ld + cr0 + lane] : 0.0;
+        }
 #pragma unroll
-          for (int q = 0; q < UNR; ++q) {
-            const int r = r0 + q * NW;
-            if (r < nr && okc) {
-              double v = x[q];
+        for (int q = 0; q < UNR; ++q) {
+          const int r = r0 + q * NW;
+          if (r < nr && lane < nc) {
+            double v = x[q];
 #pragma unroll
-              for (int k = 0; k < SPW; ++k) v = fma(-sp[r * SP_LD + k], ubuf[k * PW + col], v);
-              M[static_cast<int64_t>(c0 + r) * ld + cr0 + col] = v;
-            }
+            for (int k = 0; k < SPW; ++k) v = fma(-sp[r * SP_LD + k], ubuf[k * PB + lane], v);
+            M[static_cast<int64_t>(c0 + r) * ld + cr0 + lane] = v;
           }
         }
       }

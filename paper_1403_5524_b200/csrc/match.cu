@@ -2,7 +2,7 @@
 // The paper is silent on this step (PAPER.md:459-514 stops at R); DESIGN.md §5.2 gives the design:
 // one CTA per energy (persistent over energies, workspace slot = blockIdx.x), blocked right-looking
 // LU with partial pivoting of A on the augmented matrix [A | B_open] (outer blocks of 256 built from
-// 64-wide panels, FP64 DMMA trailing updates through the TMA pipeline of cta_la.cuh), then
+// 32-wide panels, FP64 DMMA trailing updates through the TMA pipeline of cta_la.cuh), then
 // blocked back substitution; only the n_open open columns of B are solved, closed columns of K
 // are -e_j (precondition of rmx.h; SURVEY §8(c) reading 9).
 #include "cta_la.cuh"
@@ -39,7 +39,7 @@ struct MatchSmem {
   double redv[NW];
   int redi[NW];
   int ipiv[NB];
-  double ubuf[SPW * PW];
+  double ubuf[SPW * PB];
   GemmSync gs;
 };
 
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NT, 1)
     PH_MARK(0);  // formation pass
     // ---- S4a: blocked right-looking LU with partial pivoting on [A | B_open] ----
     // Outer blocks of 256 columns made of two 128-wide sub-blocks a, b. A sub-block is factored as
-    // two 64-wide panels (the first followed by a K = 64 update of the sub-block's other columns);
+    // four 32-wide panels (each followed by a K = 32 update of the sub-block's remaining columns);
     // U12a = L11a^{-1} A12 as ONE in-place DMMA GEMM with the explicit 128 x 128 inverse (one
     // 128-row tile row) over every column right of a; sub-block b's columns are updated and factored
     // (its row interchanges run over the whole block, L21a included, while the trailing columns of
@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(NT, 1)
     // trailing update with K = 256 (C read and written once per 256 columns instead of twice).
     int singular = 0;
     auto factor_sub = [&](int c0, int Wblk, int sc0) {
-      for (int q0 = 0; q0 < Wblk; q0 += PW) {
-        const int c = c0 + q0, wq = min(PW, Wblk - q0), rem = Wblk - q0 - wq;
+      for (int q0 = 0; q0 < Wblk; q0 += PB) {
+        const int c = c0 + q0, wq = min(PB, Wblk - q0), rem = Wblk - q0 - wq;
         singular |= panel_lu(Mw, ldm, n, c, wq, sc0, ncols, sm.ipiv + q0, sm.gemm, sm.ubuf, sm.redv,
                              sm.redi);
         if (rem > 0) {
