@@ -102,6 +102,9 @@ rmx_rc rmx_build_R(rmx_ctx *ctx, const double *w, int64_t ldw, const double *Ek,
  *   K              DEVICE [ne][nch][nch] output
  *   status         DEVICE int32 [ne]: RMX_E_SINGULAR on an exact zero pivot,
  *                  RMX_E_NONFINITE if K_oo is not finite
+ * Errors: EINVAL on null pointers, sizes < 1, a <= 0, or nch > 8192 (up to 2944 channels the LU
+ * sub-panels live in shared memory, beyond in the workspace slot; the number of per-energy
+ * workspace slots is capped at 48 GB, so very large nch runs fewer energies concurrently).
  */
 rmx_rc rmx_match_K(rmx_ctx *ctx, const double *R, const double *F, const double *G,
                    const double *Fp, const double *Gp, double a, int64_t nch, int64_t ne,

@@ -66,6 +66,9 @@ __global__ void __launch_bounds__(NT, 1)
   const MatView Mv{views + (blockIdx.x * 2 + 0) * NVIEW, slot + L.m_off, ldm, n};
   const MatView Tv{views + (blockIdx.x * 2 + 1) * NVIEW, slot + L.tg_off, TG, TG};
   double *Mw = Mv.base;
+  // LU sub-panel staging: shared memory up to kSmemPanelChannels, the slot's scratch beyond (generic
+  // addressing: the same panel_lu code; __syncthreads orders the global accesses within the CTA)
+  double *spbuf = (n <= kSmemPanelChannels) ? sm.gemm : slot + L.sp_off;
   double *smg = sm.gemm;
   GemmSync *gs = &sm.gs;
 
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(NT, 1)
     auto factor_sub = [&](int c0, int Wblk, int sc0) {
       for (int q0 = 0; q0 < Wblk; q0 += PB) {
         const int c = c0 + q0, wq = min(PB, Wblk - q0), rem = Wblk - q0 - wq;
-        singular |= panel_lu(Mw, ldm, n, c, wq, sc0, ncols, sm.ipiv + q0, sm.gemm, sm.ubuf, sm.redv,
+        singular |= panel_lu(Mw, ldm, n, c, wq, sc0, ncols, sm.ipiv + q0, spbuf, sm.ubuf, sm.redv,
                              sm.redi);
         if (rem > 0) {
           // sub-block columns right of this panel: U rows = L_qq^{-1} A ; rows below -= L U

@@ -156,9 +156,14 @@ rmx_rc grow(rmx_ctx *c, void **p, size_t *have, size_t need) {
 
 rmx_rc grow(rmx_ctx *c, rmx_ctx::Dev &d, size_t need) { return grow(c, &d.p, &d.bytes, need); }
 
-// One CTA per SM (the per-energy kernels use ~220 KB of shared memory): slots = #SMs.
-int64_t ws_slots_for(const rmx_ctx *c, int64_t ne) {
-  return std::min<int64_t>(ne, static_cast<int64_t>(c->nsm));
+int64_t ws_slot_doubles(int64_t nch);
+// One CTA per SM (the per-energy kernels use ~220 KB of shared memory): slots = #SMs, fewer when the
+// slots would exceed a 48 GB budget (large nch: the T slot is 5 n^2 doubles, 2.7 GB at n = 8192); the
+// persistent kernels then loop over more energies per CTA.
+int64_t ws_slots_for(const rmx_ctx *c, int64_t nch, int64_t ne) {
+  const int64_t budget = static_cast<int64_t>(48) << 30;
+  const int64_t by_mem = std::max<int64_t>(1, budget / (ws_slot_doubles(nch) * 8));
+  return std::min<int64_t>(std::min<int64_t>(ne, static_cast<int64_t>(c->nsm)), by_mem);
 }
 
 rmx_rc build_views(rmx_ctx *c, CUtensorMap **dst, int64_t nch, int64_t slots, int64_t per_slot,
@@ -356,7 +361,7 @@ rmx_rc rmx_match_K(rmx_ctx *c, const double *R, const double *F, const double *G
   if (!(a > 0.0)) return fail(c, RMX_EINVAL, "rmx_match_K: a must be > 0");
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
-  const int64_t slots = ws_slots_for(c, ne);
+  const int64_t slots = ws_slots_for(c, nch, ne);
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   cudaError_t e = timed(c, RMX_KID_MATCH, 1, [&] {
@@ -376,7 +381,7 @@ rmx_rc rmx_collision_strength(rmx_ctx *c, const double *K, int64_t nch, int64_t 
   if (nch > (1 << 16)) return fail(c, RMX_EINVAL, "rmx_collision_strength: nch too large");
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
-  const int64_t slots = ws_slots_for(c, ne);
+  const int64_t slots = ws_slots_for(c, nch, ne);
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   cudaError_t e = timed(c, RMX_KID_TEPI, 1, [&] {
@@ -407,7 +412,7 @@ rmx_rc rmx_collision_strength_levels(rmx_ctx *c, const double *K, int64_t nch, i
   if (rc != RMX_OK) return rc;
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
-  const int64_t slots = ws_slots_for(c, ne);
+  const int64_t slots = ws_slots_for(c, nch, ne);
   rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   LevelSums lv;
@@ -426,8 +431,8 @@ rmx_rc rmx_collision_strength_levels(rmx_ctx *c, const double *K, int64_t nch, i
 static int64_t default_batch(const rmx_ctx *c, int64_t nch, int64_t ne) {
   const int64_t unit = 2 * static_cast<int64_t>(c->nsm);
   const int64_t budget = static_cast<int64_t>(8) << 30;  // bytes for the R/K batch buffer
-  int64_t b = budget / (nch * nch * 8);
-  b = std::max<int64_t>(unit, (b / unit) * unit);
+  int64_t b = std::max<int64_t>(1, budget / (nch * nch * 8));
+  if (b >= unit) b = (b / unit) * unit;  // whole waves of 2 energies per SM when the budget allows
   return std::min<int64_t>(b, ne);
 }
 
@@ -461,7 +466,7 @@ static rmx_rc sweep_impl(rmx_ctx *c, const double *w, int64_t ldw, const double 
   cudaSetDevice(c->device);
   if (batch <= 0) batch = default_batch(c, nch, ne);
   batch = std::min(batch, ne);
-  const int64_t slots = ws_slots_for(c, batch);
+  const int64_t slots = ws_slots_for(c, nch, batch);
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   const size_t mat = static_cast<size_t>(nch) * nch;
@@ -605,7 +610,7 @@ rmx_rc rmx_photoionization(rmx_ctx *c, const double *K, const double *g, const d
     return fail(c, RMX_EINVAL, "rmx_photoionization: bad sizes");
   if (check_sticky(c) != RMX_OK) return RMX_ECUDA;
   cudaSetDevice(c->device);
-  const int64_t slots = ws_slots_for(c, ne);
+  const int64_t slots = ws_slots_for(c, nch, ne);
   rmx_rc rc = ensure_ws(c, nch, slots);
   if (rc != RMX_OK) return rc;
   PhotoArgs pa;
