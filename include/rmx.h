@@ -337,6 +337,14 @@ rmx_rc rmx_stats(rmx_ctx *ctx, double *ms_per_kid /* [RMX_NKID] */,
 int rmx_version(void);
 int rmx_sm_target(void);
 
+/* Host-only query (no GPU, no context): doubles of device workspace one in-flight energy of the
+ * per-energy kernels (rmx_match_K, rmx_collision_strength*, rmx_photoionization) takes for nch
+ * channels - the larger of the matching slot ([A | B_open] n x 2n_pad, a 128 x 128 block inverse, an
+ * n x 9 LU sub-panel) and the T-epilogue slot (five n x ld_o planes and the d/v vectors), rounded up
+ * to whole 128-byte lines so every slot base is 16-byte aligned for TMA. A context holds
+ * min(#SMs, ne, 48 GB / slot) such slots. Returns -1 for nch < 1 or nch > 65536. */
+int64_t rmx_workspace_doubles_per_energy(int64_t nch);
+
 #ifdef __cplusplus
 }
 #endif

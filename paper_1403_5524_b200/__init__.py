@@ -39,7 +39,7 @@ EXPORTED = ("rmx_create", "rmx_destroy", "rmx_set_stream", "rmx_last_error", "rm
             "rmx_maxwell_average",
             "rmx_sync",
             "rmx_set_r_algo", "rmx_set_timing", "rmx_reset_stats", "rmx_stats", "rmx_version",
-            "rmx_sm_target")
+            "rmx_sm_target", "rmx_workspace_doubles_per_energy")
 
 
 class RmxError(RuntimeError):
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rmx_last_error.restype = ctypes.c_char_p
     lib.rmx_version.restype = ctypes.c_int
     lib.rmx_sm_target.restype = ctypes.c_int
+    lib.rmx_workspace_doubles_per_energy.argtypes = [ctypes.c_int64]
+    lib.rmx_workspace_doubles_per_energy.restype = ctypes.c_int64
     _lib = lib
     return lib
 

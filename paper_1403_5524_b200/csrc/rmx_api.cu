@@ -193,7 +193,9 @@ rmx_rc build_views(rmx_ctx *c, CUtensorMap **dst, int64_t nch, int64_t slots, in
 }
 
 int64_t ws_slot_doubles(int64_t nch) {
-  return std::max(match_ws_doubles_per_slot(nch), tepi_ws_doubles_per_slot(nch));
+  // whole 128-byte lines, so that every slot base keeps the 16-byte alignment TMA needs
+  const int64_t d = std::max(match_ws_doubles_per_slot(nch), tepi_ws_doubles_per_slot(nch));
+  return (d + 15) & ~15LL;
 }
 
 // Workspace for `slots` per-energy slots of the matching / T kernels, with their TMA views.
@@ -230,6 +232,10 @@ extern "C" {
 
 int rmx_version(void) { return 200; }
 int rmx_sm_target(void) { return 100; }
+int64_t rmx_workspace_doubles_per_energy(int64_t nch) {
+  if (nch < 1 || nch > (1 << 16)) return -1;
+  return ws_slot_doubles(nch);
+}
 
 rmx_rc rmx_create(rmx_ctx **ctx, int device, void *stream) {
   if (!ctx) return RMX_EINVAL;

@@ -31,7 +31,7 @@ __host__ __device__ inline MatchLayout match_layout(int64_t nch) {
   L.m_off = 0;
   L.tg_off = nch * L.ldm + 32;
   L.sp_off = L.tg_off + 128 * 128 + 32;  // Tg: inverse of a 128 x 128 diagonal block
-  L.slot = L.sp_off + nch * 9 + 32;      // LU sub-panel (n x 9) when it exceeds shared memory
+  L.slot = L.sp_off + ((9 * nch + 1) & ~1LL) + 32;  // LU sub-panel (n x 9) beyond shared memory
   return L;
 }
 // T epilogue (tepi.cu): five planes [nch][ldo] (Ar, Ai, Yr, Yi, P) and the vectors d (re, im), v

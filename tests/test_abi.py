@@ -77,3 +77,18 @@ def test_sass_is_sm100a_with_dmma_and_tma(lib):
     assert "DMMA.8x8x4" in sass          # FP64 tensor-core MMA in R formation / LU / Cholesky
     assert "UTMALDG" in sass             # TMA tile loads (cp.async.bulk.tensor) in R formation
     assert "UBLKCP" in sass              # cp.async.bulk C-tile copies in the per-energy dense LA
+
+
+def test_workspace_slot_layout(lib):
+    """Host-only layout query: every per-energy slot base must stay 16-byte aligned for the TMA
+    tensor maps built on it (an odd slot size broke rmx_match_K at nch = 37), and a slot must hold
+    what the kernels write - the matching [A | B_open] block (n x 2n) and the five T planes."""
+    f = lib.rmx_workspace_doubles_per_energy
+    assert f(0) == -1 and f(-5) == -1 and f((1 << 16) + 1) == -1
+    prev = 0
+    for n in list(range(1, 300)) + [511, 512, 513, 1200, 2000, 2944, 2945, 3500, 8192]:
+        d = f(n)
+        assert d % 16 == 0, (n, d)
+        assert d >= 2 * n * n + 9 * n and d >= 5 * n * n, (n, d)
+        assert d >= prev  # monotone in nch: a context grown for n serves every smaller n
+        prev = d
