@@ -32,10 +32,12 @@ def _stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build_phases(verbose: bool = False) -> str:
-    """Diagnostic variant with per-phase clock64 counters in the matching kernel (librmx_phases.so)."""
-    out = os.path.join(PKG, "librmx_phases.so")
-    cmd = [NVCC, *FLAGS, "-DRMX_PHASES", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
+def build_phases(verbose: bool = False, suffix: str = "", defines=()) -> str:
+    """Diagnostic variant with per-phase clock64 counters in the matching kernel (librmx_phases.so);
+    suffix/defines build A/B variants (librmx_phases<suffix>.so with extra -D flags)."""
+    out = os.path.join(PKG, f"librmx_phases{suffix}.so")
+    cmd = [NVCC, *FLAGS, "-DRMX_PHASES", *[f"-D{d}" for d in defines], "-o", out,
+           *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd, cwd=CSRC)
@@ -70,7 +72,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     if "--phases" in sys.argv:
-        print(build_phases(verbose=True))
+        # --phases [SUFFIX DEFINE ...]: an A/B variant of the diagnostic build
+        rest = sys.argv[sys.argv.index("--phases") + 1:]
+        print(build_phases(verbose=True, suffix=rest[0] if rest else "", defines=rest[1:]))
     elif "--checked" in sys.argv:
         print(build_checked(force=True, verbose=True))
     else:

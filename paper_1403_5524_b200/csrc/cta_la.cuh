@@ -465,15 +465,40 @@ __device__ __forceinline__ void block_argmax(double &v, int &idx, double *redv, 
 // order, and the panel's remaining columns get one rank-8 update pass (U rows by a unit-lower 8x8
 // solve). Global memory is touched ~4 times per 32 columns instead of once per column.
 constexpr int SPW = 8, SP_LD = SPW + 1;
+constexpr int PERM_MAX = 2 * PB;
+#ifdef RMX_PHASES
+// panel_lu sub-step clock64 totals of block 0 (diagnostic build; rmx_debug_panel_phases)
+static __device__ unsigned long long g_panel_phase[6];
+#define PANEL_MARK(k)                                   \
+  do {                                                  \
+    __syncthreads();                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {          \
+      const unsigned long long now_ = clock64();        \
+      g_panel_phase[k] += now_ - pp_t0;                 \
+      pp_t0 = now_;                                     \
+    }                                                   \
+  } while (0)
+#else
+#define PANEL_MARK(k) \
+  do {                \
+  } while (0)
+#endif
+#ifndef RMX_PANEL_SU
+#define RMX_PANEL_SU 16
+#endif
+  // rows touched by the interchanges of one panel
+
 __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, int bw, int sc0,
                                         int sc1, int *ipiv, double *sp, double *ubuf, double *redv,
                                         int *redi) {
-  const int warp = warp_id(), lane = lane_id();
   int singular = 0;
+#ifdef RMX_PHASES
+  unsigned long long pp_t0 = clock64();
+#endif
   for (int s0 = 0; s0 < bw; s0 += SPW) {
     const int c0 = p0 + s0, w = min(SPW, bw - s0), nr = n - c0;
     // 1. stage the sub-panel rows c0..n-1, columns c0..c0+w (SU loads in flight per thread)
-    constexpr int SU = 8;
+    constexpr int SU = RMX_PANEL_SU;
     __syncthreads();
     for (int q0 = threadIdx.x; q0 < nr * SPW; q0 += NT * SU) {
       double v[SU];
@@ -489,17 +514,19 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
       }
     }
     __syncthreads();
-    // 2. factor in shared memory
-    for (int jj = 0; jj < w; ++jj) {
-      double best = -1.0;
-      int besti = nr;
-      for (int r = jj + threadIdx.x; r < nr; r += NT) {
-        const double v = fabs(sp[r * SP_LD + jj]);
-        if (v > best) {
-          best = v;
-          besti = r;
-        }
+    PANEL_MARK(0);
+    // 2. factor in shared memory; each column's rank-1 update pass also searches the next
+    // column's pivot (one pass over the rows and one barrier per column fewer)
+    double best = -1.0;
+    int besti = nr;
+    for (int r = threadIdx.x; r < nr; r += NT) {
+      const double v = fabs(sp[r * SP_LD]);
+      if (v > best) {
+        best = v;
+        besti = r;
       }
+    }
+    for (int jj = 0; jj < w; ++jj) {
       block_argmax(best, besti, redv, redi);
       const int pr = besti < nr ? besti : jj;  // all-NaN column (e.g. a pole energy): no interchange
       if (threadIdx.x < SPW && pr != jj) {
@@ -516,22 +543,35 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
       double u[SPW];
 #pragma unroll
       for (int q = 0; q < SPW; ++q) u[q] = sp[jj * SP_LD + q];
-      for (int r = jj + 1 + threadIdx.x; r < nr; r += NT) {
+      const int jn = jj + 1;  // next pivot column (searched over rows >= jn)
+      best = -1.0;
+      besti = nr;
+      for (int r = jn + threadIdx.x; r < nr; r += NT) {
         double *row = sp + r * SP_LD;
         const double l = zero ? 0.0 : row[jj] * rpiv;
         if (!zero) row[jj] = l;
 #pragma unroll
         for (int q = 0; q < SPW; ++q)
           if (q > jj) row[q] = fma(-l, u[q], row[q]);
+        if (jn < w) {
+          const double v = fabs(row[jn]);
+          if (v > best) {
+            best = v;
+            besti = r;
+          }
+        }
       }
-      __syncthreads();
     }
+    __syncthreads();
+    PANEL_MARK(1);
     // 3. write the factored sub-panel back
     for (int q = threadIdx.x; q < nr * SPW; q += NT) {
       const int r = q / SPW, c = q % SPW;
       if (c < w) M[static_cast<int64_t>(c0 + r) * ld + c0 + c] = sp[r * SP_LD + c];
     }
-    // 4. the sub-panel's interchanges, in order, on the rest of the augmented rows
+    // 4. the sub-panel's interchanges, in order, on the rest of the augmented rows (a composed
+    // permutation of the panel's rows, applied once per panel, measured slower: the pass is bound by
+    // the rows' bytes)
     for (int jj = 0; jj < w; ++jj) {
       const int pr = ipiv[s0 + jj], j = c0 + jj;
       RMX_CHECK(pr >= j && pr < n && sc1 <= ld);
@@ -560,6 +600,7 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
       }
       __syncthreads();
     }
+    PANEL_MARK(2);
     // 5. rank-w update of the panel's remaining columns [c0+w, p0+bw)
     const int cr0 = c0 + w, nc = p0 + bw - cr0;
     if (nc > 0) {
@@ -581,27 +622,30 @@ __device__ __forceinline__ int panel_lu(double *M, int64_t ld, int n, int p0, in
         }
       }
       __syncthreads();
-      // rows c0+w..n-1: M[i][c] -= sum_q L[i][q] U[q][c]; warp per row, lane per column
-      constexpr int UNR = 8;
-      for (int r0 = w + warp; r0 < nr; r0 += NW * UNR) {
+      // rows c0+w..n-1: M[i][c] -= sum_q L[i][q] U[q][c]; (row, column) elements dealt to all
+      // threads, UNR independent loads in flight per thread (the pass is latency-bound)
+      constexpr int UNR = 16;
+      const int tot = (nr - w) * nc;
+      for (int q0 = threadIdx.x; q0 < tot; q0 += NT * UNR) {
         double x[UNR];
 #pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-          const int r = r0 + q * NW;
-          x[q] = (r < nr && lane < nc) ? M[static_cast<int64_t>(c0 + r) * ld + cr0 + lane] : 0.0;
+        for (int u = 0; u < UNR; ++u) {
+          const int q = q0 + u * NT, r = w + q / nc, c = q % nc;
+          x[u] = q < tot ? M[static_cast<int64_t>(c0 + r) * ld + cr0 + c] : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-          const int r = r0 + q * NW;
-          if (r < nr && lane < nc) {
-            double v = x[q];
+        for (int u = 0; u < UNR; ++u) {
+          const int q = q0 + u * NT, r = w + q / nc, c = q % nc;
+          if (q < tot) {
+            double v = x[u];
 #pragma unroll
-            for (int k = 0; k < SPW; ++k) v = fma(-sp[r * SP_LD + k], ubuf[k * PB + lane], v);
-            M[static_cast<int64_t>(c0 + r) * ld + cr0 + lane] = v;
+            for (int k = 0; k < SPW; ++k) v = fma(-sp[r * SP_LD + k], ubuf[k * PB + c], v);
+            M[static_cast<int64_t>(c0 + r) * ld + cr0 + c] = v;
           }
         }
       }
     }
+    PANEL_MARK(3);
   }
   __syncthreads();
   return singular;

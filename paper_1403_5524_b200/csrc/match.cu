@@ -7,6 +7,7 @@
 // are -e_j (precondition of rmx.h; SURVEY §8(c) reading 9).
 #include "cta_la.cuh"
 #include "rmx_internal.h"
+#include <cstdlib>
 
 namespace rmx {
 
@@ -245,6 +246,11 @@ int64_t match_ws_doubles_per_slot(int64_t nch) { return match_layout(nch).slot; 
 extern "C" int rmx_debug_match_phases(unsigned long long *out) {
   cudaDeviceSynchronize();
   return static_cast<int>(cudaMemcpyFromSymbol(out, g_match_phase, sizeof(g_match_phase)));
+}
+// panel_lu sub-steps: staging, factor, write-back + interchanges, rank-w update
+extern "C" int rmx_debug_panel_phases(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  return static_cast<int>(cudaMemcpyFromSymbol(out, la::g_panel_phase, 6 * sizeof(unsigned long long)));
 }
 #endif
 

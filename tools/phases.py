@@ -28,6 +28,10 @@ names = ["formation", "panels (panel_lu + K=32 updates)", "U12 + K=128 trailing"
 tot = sum(out[k] for k in range(7))
 for k, n in enumerate(names):
     print(f"{n:36s} {out[k] / 1e6:10.1f} Mcycles {100 * out[k] / tot:5.1f} %")
+if hasattr(ctx.lib, "rmx_debug_panel_phases"):
+    ctx.lib.rmx_debug_panel_phases(out)
+    for k, n in enumerate(["staging", "factor (smem)", "write-back + interchanges", "rank-w update"]):
+        print(f"  panel {n:30s} {out[k] / 1e6:10.1f} Mcycles")
 # T epilogue (tepi.cu, complex LDL^T route)
 ctx.lib.rmx_debug_tepi_phases(out)
 names = ["copy (+ photo v)", "diagonal LDL^T + inverse (smem)", "W21 = A21 Tinv^T", "L21 scaling",
