@@ -184,15 +184,28 @@ __global__ void __launch_bounds__(NT, 1)
     // rmx_match_K); the blocks and the update order of rows >= nc are the same either way, so
     // K_oo is bitwise identical in both modes
     const int rlo = open_rows_only ? nc : 0;
+    // 128-row blocks taken in pairs (a above b) from the bottom, the pairing independent of rlo:
+    // Y_b = U_bb^{-1} Y_b; Y_a -= U_ab Y_b; Y_a = U_aa^{-1} Y_a; then ONE update of the rows above
+    // the pair with K = 256 (the C rows read and written once per 256 solved rows)
     if (o > 0) {
-      for (int P0 = ((n - 1) / NB) * NB; P0 >= 0 && P0 + NB > rlo; P0 -= NB) {
-        const int W = min(NB, n - P0);
+      for (int Pb = ((n - 1) / NB) * NB; Pb >= 0 && Pb + NB > rlo; Pb -= 2 * NB) {
+        const int Wb = min(NB, n - Pb), Pa = Pb - NB;
+        const bool has_a = Pa >= 0 && Pa + NB > rlo;
         PH_MARK(3);
-        tri_inv128(Mv, P0, W, TRI_UPPER, Tv, smg, gs);  // U_pp^{-1}
+        tri_inv128(Mv, Pb, Wb, TRI_UPPER, Tv, smg, gs);  // U_bb^{-1}
         PH_MARK(6);
-        gemm_set(W, o, W, opk(Tv, 0, 0), opn(Mv, P0, npad), Mv, P0, npad, false, 0.0, smg, gs);
-        if (P0 > rlo)
-          gemm_sub(P0 - rlo, o, W, opk(Mv, rlo, P0), opn(Mv, P0, npad), Mv, rlo, npad, false, smg, gs);
+        gemm_set(Wb, o, Wb, opk(Tv, 0, 0), opn(Mv, Pb, npad), Mv, Pb, npad, false, 0.0, smg, gs);
+        if (has_a) {
+          gemm_sub(NB, o, Wb, opk(Mv, Pa, Pb), opn(Mv, Pb, npad), Mv, Pa, npad, false, smg, gs);
+          PH_MARK(3);
+          tri_inv128(Mv, Pa, NB, TRI_UPPER, Tv, smg, gs);  // U_aa^{-1}
+          PH_MARK(6);
+          gemm_set(NB, o, NB, opk(Tv, 0, 0), opn(Mv, Pa, npad), Mv, Pa, npad, false, 0.0, smg, gs);
+          if (Pa > rlo)
+            gemm_sub(Pa - rlo, o, NB + Wb, opk(Mv, rlo, Pa), opn(Mv, Pa, npad), Mv, rlo, npad, false, smg, gs);
+        } else if (Pb > rlo) {
+          gemm_sub(Pb - rlo, o, Wb, opk(Mv, rlo, Pb), opn(Mv, Pb, npad), Mv, rlo, npad, false, smg, gs);
+        }
       }
     }
 
