@@ -112,15 +112,25 @@ __device__ __noinline__ int tiled_t2(const double *P, const double *X, int64_t l
     }
     const int bj = rem;
     const bool diag = bi == bj;
-    for (int r = 0; r < 32; ++r) {
-      const int gi = bi * 32 + r, gj = bj * 32 + lane;
-      double v = 0.0;
-      if (gi < o && gj < o && (!diag || lane <= r)) {
-        const double x = X[static_cast<int64_t>(gi) * ld + gj];
-        const double pv = (gi == gj ? 1.0 : 0.0) - P[static_cast<int64_t>(gi) * ld + gj];
-        v = 4.0 * fma(x, x, pv * pv);
+    for (int r0 = 0; r0 < 32; r0 += 8) {  // 16 independent loads in flight per lane
+      double xv[8], pv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u, gi = bi * 32 + r, gj = bj * 32 + lane;
+        const bool ok = gi < o && gj < o && (!diag || lane <= r);
+        xv[u] = ok ? X[static_cast<int64_t>(gi) * ld + gj] : 0.0;
+        pv[u] = ok ? P[static_cast<int64_t>(gi) * ld + gj] : 0.0;
       }
-      tile[r * TL + lane] = v;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u, gi = bi * 32 + r, gj = bj * 32 + lane;
+        double v = 0.0;
+        if (gi < o && gj < o && (!diag || lane <= r)) {
+          const double p = (gi == gj ? 1.0 : 0.0) - pv[u];
+          v = 4.0 * fma(xv[u], xv[u], p * p);
+        }
+        tile[r * TL + lane] = v;
+      }
     }
     __syncwarp();
     if (diag)
@@ -434,18 +444,30 @@ __global__ void __launch_bounds__(NT, 1)
         const double ir = a / den, ii = -b / den;
         double *zr = Arv.at(i, 0), *zi = Aiv.at(i, 0), *yr = Yrv.at(i, 0), *yi = Yiv.at(i, 0);
         const int zend = min(o, (i / (2 * CB) + 1) * (2 * CB));
-        for (int j = lane_id(); j < o; j += 32) {
-          if (j <= i) {
-            const double xr = zr[j], xi = zi[j];
-            yr[j] = xr * ir - xi * ii;
-            yi[j] = fma(xr, ii, xi * ir);
-          } else {
-            yr[j] = 0.0;
-            yi[j] = 0.0;
-            if (j < zend) {
-              zr[j] = 0.0;
-              zi[j] = 0.0;
+        constexpr int U = 8;  // 2U independent loads in flight per lane (the pass is latency-bound)
+        for (int j0 = lane_id(); j0 <= i; j0 += 32 * U) {
+          double xr[U], xi[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + 32 * u;
+            xr[u] = j <= i ? zr[j] : 0.0;
+            xi[u] = j <= i ? zi[j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + 32 * u;
+            if (j <= i) {
+              yr[j] = xr[u] * ir - xi[u] * ii;
+              yi[j] = fma(xr[u], ii, xi[u] * ir);
             }
+          }
+        }
+        for (int j = i + 1 + lane_id(); j < o; j += 32) {
+          yr[j] = 0.0;
+          yi[j] = 0.0;
+          if (j < zend) {
+            zr[j] = 0.0;
+            zi[j] = 0.0;
           }
         }
       }
