@@ -299,6 +299,191 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+// ---------------------------------------------------------------------------------------------
+// The same conversion with the byte-weight sums on the tensor cores (the default for unsigned X
+// residues; oz_convert_kernel above stays for balanced residues, nlev > 65000, and as the
+// RMX_I8_CONV_ALU A/B switch). Per (row i, 1024 k) work item and energy each of the 128 threads
+// forms u = X' + 2^54 for 8 consecutive k as in oz_convert_kernel and writes its 8 bytes plus a
+// constant 1 in byte 7 (u < 2^56) to shared-memory row t (SWIZZLE_128B K-major, 32 K-bytes = 4
+// elements per MMA K-slice); one tcgen05.mma.kind::i8 (M = 128, N = 64, K = 32, u8 x u8 -> s32) per
+// slice against the block-diagonal weight matrix B[16q + l][8q + b] = 2^{8b} mod m_l (b < 7),
+// (-2^54) mod m_l (b = 7) gives sv_l = sum_b byte_b (2^{8b} mod m_l) + (-2^54 mod m_l) < 2^19 for
+// the 4 elements q and the 16 moduli l - exactly the two dp4a of oz_convert_kernel - in TMEM column
+// 64 s + 16 q + l of lane t. The ALUs are left with the 15 reductions sv mod m (multiply-high) and the
+// byte packing: half the integer-pipe instructions per element. Bitwise the same
+// residues as oz_convert_kernel (tests/test_rint8.py: R bitwise equal under both).
+constexpr int CT_NT = 128, CT_EL = 8, CT_K = CT_NT * CT_EL;   // k per work item
+constexpr int CT_A_BYTES = 128 * 128, CT_B_BYTES = 64 * 128;  // SW128 tiles (A: 2 of 4 slices used)
+constexpr int CT_SMEM = 1024 + CT_A_BYTES + CT_B_BYTES + 64;
+// 128 registers x 128 threads cap residency at 4 CTAs per SM = 4 x 128 TMEM columns; the small shared
+// footprint lets a conversion CTA sit beside a pair-GEMM CTA whose ring leaves room (RMX_I8_STAGES)
+constexpr int CT_SMEM_REQ = (1024 + CT_A_BYTES + CT_B_BYTES + 64 + 127) / 128 * 128;
+constexpr int CT_TMEM_COLS = 128;       // 2 slices x N = 64
+static_assert(CT_SMEM <= CT_SMEM_REQ, "conversion tiles exceed the requested shared memory");
+constexpr uint32_t CT_IDESC = (2u << 4) | (static_cast<uint32_t>(64 >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t ct_weight(int l, int b) {
+  const ModConst &mc = c_mod[l];
+  if (b < 4) return (mc.blo >> (8 * b)) & 0xFFu;
+  if (b < 7) return (mc.bhi >> (8 * (b - 4))) & 0xFFu;
+  return mc.boff;
+}
+
+__global__ void __launch_bounds__(CT_NT, 4)
+    oz_convert_tc_kernel(const double *__restrict__ w, int64_t ldw, int nch, int nlev, int ne,
+                         const double *__restrict__ dbuf, const float *__restrict__ xmax, int bits, int64_t ldv,
+                         int8_t *__restrict__ out, int32_t *__restrict__ shift, int items_per_cta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *As = smem, *Bs = smem + CT_A_BYTES;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(Bs + CT_B_BYTES);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
+  const int t = threadIdx.x, warp = warp_id();
+  // weight tile: row n (= 16 q + l), K bytes 0..31 of 128 (SW128: 16-byte chunk c at c ^ (n & 7))
+  for (int idx = t; idx < 64 * 8; idx += CT_NT) {
+    const int n = idx >> 3, c = idx & 7;
+    uint32_t v[4] = {0u, 0u, 0u, 0u};
+    if (c < 2) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int kk = 16 * c + j;
+        if ((kk >> 3) == (n >> 4)) v[j >> 2] |= ct_weight(n & 15, kk & 7) << (8 * (j & 3));
+      }
+    }
+    *reinterpret_cast<uint4 *>(Bs + n * 128 + ((c ^ (n & 7)) * 16)) = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(CT_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_proxy_async();
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a_base = smem_u32(As), b_base = smem_u32(Bs);
+  uint8_t *arow = As + t * 128;
+  const int sw = t & 7;
+  const int nkb = (nlev + CT_K - 1) / CT_K;
+  const int64_t nitems = static_cast<int64_t>(nch) * nkb;
+  const int64_t plane = static_cast<int64_t>(nch) * ldv;
+  const uint64_t bias = (static_cast<uint64_t>(1) << BX) | (static_cast<uint64_t>(1) << 56);  // + byte 7 = 1
+  uint32_t phase = 0;
+  const int64_t it0 = static_cast<int64_t>(blockIdx.x) * items_per_cta;
+  const int64_t it1 = min(nitems, it0 + items_per_cta);
+  for (int64_t it = it0; it < it1; ++it) {
+    const int i = static_cast<int>(it / nkb), kb = static_cast<int>(it % nkb);
+    const int k0 = kb * CT_K + t * CT_EL;
+    double wv[CT_EL];
+    const double *wr = w + static_cast<int64_t>(i) * ldw + k0;
+#pragma unroll
+    for (int q = 0; q < CT_EL; ++q) wv[q] = (k0 + q < nlev) ? wr[q] : 0.0;
+    // d and the row bound of energy e + 1 are loaded while energy e is converted (latency-bound
+    // otherwise: ncu long-scoreboard stalls on these loads dominated the first version; prefetching
+    // the next work item's W as well spilled and measured slower)
+    double dcur[CT_EL];
+    float bcur = xmax[i];
+#pragma unroll
+    for (int q = 0; q < CT_EL; ++q) dcur[q] = (k0 + q < nlev) ? dbuf[k0 + q] : 0.0;
+    for (int e = 0; e < ne; ++e) {
+      double dnext[CT_EL];
+      float bnext = 0.0f;
+      if (e + 1 < ne) {
+        const double *dn = dbuf + static_cast<int64_t>(e + 1) * nlev + k0;
+        bnext = xmax[static_cast<int64_t>(e + 1) * nch + i];
+#pragma unroll
+        for (int q = 0; q < CT_EL; ++q) dnext[q] = (k0 + q < nlev) ? dn[q] : 0.0;
+      }
+      const double bound = static_cast<double>(bcur);
+      int ex = 0;
+      if (bound > 0.0 && isfinite(bound)) frexp(bound, &ex);
+      const int s = bits - ex;
+      const double scale = ldexp(1.0, s);
+      if (kb == 0 && t == 0) shift[static_cast<int64_t>(e) * nch + i] = s;
+      uint64_t u[CT_EL];
+#pragma unroll
+      for (int q = 0; q < CT_EL; ++q) {
+        double x = wv[q] * dcur[q];
+        x *= scale;
+        if (!isfinite(x)) x = 0.0;  // pole energies: R is NaN anyway (status POLE)
+        u[q] = static_cast<uint64_t>(__double2ll_rn(x)) + bias;
+      }
+      // row t: 16-byte chunk c (elements 2c, 2c+1) at chunk c ^ (t & 7)
+#pragma unroll
+      for (int c = 0; c < CT_EL / 2; ++c)
+        *reinterpret_cast<uint4 *>(arow + ((c ^ sw) * 16)) =
+            make_uint4(static_cast<uint32_t>(u[2 * c]), static_cast<uint32_t>(u[2 * c] >> 32),
+                       static_cast<uint32_t>(u[2 * c + 1]), static_cast<uint32_t>(u[2 * c + 1] >> 32));
+      fence_proxy_async();
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      __syncthreads();
+      if (t == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const uint64_t db = umma_desc_sw128(b_base);
+#pragma unroll
+        for (int sl = 0; sl < CT_EL / 4; ++sl) {
+          const uint64_t da = umma_desc_sw128(a_base) + 2 * sl;  // K-bytes 32 sl .. 32 sl + 31
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + 64u * sl),
+                       "l"(da), "l"(db), "r"(CT_IDESC), "r"(0));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(bar))
+                     : "memory");
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      uint32_t pk[L][CT_EL / 4];
+#pragma unroll
+      for (int sl = 0; sl < CT_EL / 4; ++sl) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // TMEM columns 64 sl + 16 q + l: element 4 sl + q, modulus l
+          uint32_t v[16];
+          const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + 64u * sl + 16u * q;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            uint32_t r = v[l];
+            if (l > 0) {  // sv mod m (sv < 2^19: umulhi by ceil(2^32/m) is floor(sv/m) exactly)
+              const uint32_t m = static_cast<uint32_t>(mod_of(l));
+              r -= __umulhi(r, c_mod[l].magic) * m;
+            }
+            // byte q of the word (little-endian: element k0 + 4 sl + q)
+            if (q == 0)
+              pk[l][sl] = r;
+            else
+              pk[l][sl] = __byte_perm(pk[l][sl], r, q == 1 ? 0x3240 : (q == 2 ? 0x3410 : 0x4210));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      if (k0 < nlev) {
+        int8_t *o = out + static_cast<int64_t>(e) * L * plane + static_cast<int64_t>(i) * ldv + k0;
+#pragma unroll
+        for (int l = 0; l < L; ++l) *reinterpret_cast<uint2 *>(o + l * plane) = make_uint2(pk[l][0], pk[l][1]);
+      }
+#pragma unroll
+      for (int q = 0; q < CT_EL; ++q) dcur[q] = dnext[q];
+      bcur = bnext;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(CT_TMEM_COLS));
+}
+
 // GEMM epilogue of one CTA (warps 4..7): TMEM lane quarter q holds output rows row0 + q*32 + lane,
 // columns col0 .. col0 + BN - 1 in TMEM columns 0..BN-1; C mod m_l -> uint8 residue plane
 // res[e][l][row][col] (rows >= nch and column groups starting at or past nch are not stored).
@@ -435,9 +620,8 @@ __global__ void __launch_bounds__(GEMM_NT, 1)
 // throughput under the power cap +6 %, tools/tc_i8_gemm2.cu). Both CTAs' TMA completions count on the
 // leader's full barrier; the leader's single MMA thread commits each stage to both CTAs' empty
 // barriers and the finished accumulator to both accf barriers; each CTA drains its own TMEM rows.
-constexpr int P_STAGES = 7;
 constexpr int P_B_BYTES = (BN / 2) * BKB, P_STAGE_BYTES = A_BYTES + P_B_BYTES;
-constexpr int GEMM2_SMEM = 1024 + P_STAGES * P_STAGE_BYTES + 256;
+__host__ __device__ constexpr int gemm2_smem(int stages) { return 1024 + stages * P_STAGE_BYTES + 256; }
 __host__ __device__ constexpr uint32_t idesc_i8_pair(bool a_signed) {
   return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
          (static_cast<uint32_t>(256 >> 4) << 24);
@@ -456,6 +640,7 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+template <int P_STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_NT, 1)
     oz_gemm2_kernel(const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tu2,
                     const __grid_constant__ CUtensorMap tun, int nch, int nlev, int ntiles,
@@ -782,8 +967,19 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   if (ce != cudaSuccess) return ce;
   ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm_kernel), i8::GEMM_SMEM);
   if (ce != cudaSuccess) return ce;
-  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel), i8::GEMM2_SMEM);
+  // ring depth of the pair GEMM: 7 stages fill the SM's shared memory; RMX_I8_STAGES=6 / 5 leave room
+  // for one / two conversion CTAs beside it (A/B switch)
+  const char *stg_env = getenv("RMX_I8_STAGES");
+  const int p_stages = stg_env ? std::max(5, std::min(7, atoi(stg_env))) : 7;
+  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel<7>), i8::gemm2_smem(7));
+  if (ce == cudaSuccess) ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel<6>), i8::gemm2_smem(6));
+  if (ce == cudaSuccess) ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel<5>), i8::gemm2_smem(5));
   if (ce != cudaSuccess) return ce;
+  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_convert_tc_kernel), i8::CT_SMEM_REQ);
+  if (ce != cudaSuccess) return ce;
+  // X residues: byte-weight sums on the tensor cores (oz_convert_tc_kernel) unless RMX_I8_CONV_ALU is
+  // set (A/B switch; read per call so that a test can compare both in one process)
+  const bool conv_alu = getenv("RMX_I8_CONV_ALU") != nullptr;
   const int64_t ldv = rint8_ldv(nlev), ldr = rint8_ldr(nch);
   uint8_t *wsp = static_cast<uint8_t *>(ws);
   auto carve = [&](size_t bytes) {
@@ -885,7 +1081,13 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
                            0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
                                     static_cast<int>(std::min<int64_t>(8, n - q)), dbuf[b] + q * nlev,
                                     xmax[b] + q * nch);
-    if (x_signed)
+    if (!x_signed && !conv_alu) {
+      const int64_t nitems = nch * ((nlev + i8::CT_K - 1) / i8::CT_K);
+      const int ipc = 4;  // work items (row, 1024 k) per CTA (16: 8.4 waves, slower)
+      i8::oz_convert_tc_kernel<<<static_cast<unsigned>((nitems + ipc - 1) / ipc), i8::CT_NT, i8::CT_SMEM_REQ, cs>>>(
+          w, ldw, static_cast<int>(nch), static_cast<int>(nlev), static_cast<int>(n), dbuf[b], xmax[b], i8::BX,
+          ldv, V[b], sx[b], ipc);
+    } else if (x_signed)
       i8::oz_convert_kernel<true><<<g, 256, 0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
                                                          static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX, ldv,
                                                          V[b], sx[b]);
@@ -906,10 +1108,19 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
       i8::oz_gemm_kernel<<<static_cast<unsigned>(ntiles * i8::L * n), i8::GEMM_NT, i8::GEMM_SMEM, st>>>(
           tv[b], tu, static_cast<int>(nch), static_cast<int>(nlev), ntiles, tiles, ldr, res, idesc,
           static_cast<int>(n));
-    if (npair > 0)
-      i8::oz_gemm2_kernel<<<static_cast<unsigned>(2 * npair * i8::L * n), i8::GEMM_NT, i8::GEMM2_SMEM, st>>>(
-          tv[b], tu2, tun, static_cast<int>(nch), static_cast<int>(nlev), npair, tiles + ntiles, ldr, res, idesc2,
-          static_cast<int>(n), jlast, nlast);
+    if (npair > 0) {
+      const unsigned g2 = static_cast<unsigned>(2 * npair * i8::L * n);
+      const int nn = static_cast<int>(nch), nl = static_cast<int>(nlev), ne_c = static_cast<int>(n);
+      if (p_stages == 7)
+        i8::oz_gemm2_kernel<7><<<g2, i8::GEMM_NT, i8::gemm2_smem(7), st>>>(tv[b], tu2, tun, nn, nl, npair, tiles + ntiles,
+                                                                           ldr, res, idesc2, ne_c, jlast, nlast);
+      else if (p_stages == 6)
+        i8::oz_gemm2_kernel<6><<<g2, i8::GEMM_NT, i8::gemm2_smem(6), st>>>(tv[b], tu2, tun, nn, nl, npair, tiles + ntiles,
+                                                                           ldr, res, idesc2, ne_c, jlast, nlast);
+      else
+        i8::oz_gemm2_kernel<5><<<g2, i8::GEMM_NT, i8::gemm2_smem(5), st>>>(tv[b], tu2, tun, nn, nl, npair, tiles + ntiles,
+                                                                           ldr, res, idesc2, ne_c, jlast, nlast);
+    }
     gemm_mark(false);
     const int64_t ntc = (nch + 31) / 32;
     dim3 gc(static_cast<unsigned>(ntc * (ntc + 1) / 2), static_cast<unsigned>(n));

@@ -199,3 +199,27 @@ def test_int8_crt_worst_case_magnitude(ctx):
     for p, x in enumerate(E):
         ref, _ = oracle.R(w, Ek, 12.0, x, threads=oracle.default_threads())
         assert nrel(R[p], ref) < 1e-12, (x, nrel(R[p], ref))
+
+
+@pytest.mark.parametrize("nch,nlev,seed", [(300, 1000, 11), (529, 2100, 12), (257, 77, 13), (640, 4096, 14),
+                                           (384, 1023, 15)])
+def test_int8_tc_conversion_bitwise(ctx, nch, nlev, seed, monkeypatch):
+    """The X-residue conversion with the byte-weight sums on the tensor cores (oz_convert_tc_kernel, the
+    default) and the dp4a conversion (oz_convert_kernel, RMX_I8_CONV_ALU) compute the same exact
+    residues of X' = rint(w d 2^s) (DESIGN.md §5.5 step 2), so R must be bitwise equal; both are held
+    to the oracle too. nlev spans one and several 1024-k work items, ragged tails included."""
+    import torch
+    c = syn.brute_force_case(nch, nlev, seed, ne=9, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
+    monkeypatch.delenv("RMX_I8_CONV_ALU", raising=False)
+    R_tc, st1 = ctx.build_R(c.w, c.Ek, c.a, c.E)
+    torch.cuda.synchronize()
+    R_tc = R_tc.cpu().numpy()
+    monkeypatch.setenv("RMX_I8_CONV_ALU", "1")
+    R_alu, st2 = ctx.build_R(c.w, c.Ek, c.a, c.E)
+    torch.cuda.synchronize()
+    R_alu = R_alu.cpu().numpy()
+    assert np.all(st1.cpu().numpy() == 0) and np.all(st2.cpu().numpy() == 0)
+    assert np.array_equal(R_tc, R_alu)
+    for p in (0, c.ne // 2, c.ne - 1):
+        ref, _ = oracle.R(c.w, c.Ek, c.a, c.E[p])
+        assert nrel(R_tc[p], ref) < 1e-12
