@@ -312,13 +312,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 // 64 s + 16 q + l of lane t. The ALUs are left with the 15 reductions sv mod m (multiply-high) and the
 // byte packing: half the integer-pipe instructions per element. Bitwise the same
 // residues as oz_convert_kernel (tests/test_rint8.py: R bitwise equal under both).
-constexpr int CT_NT = 128, CT_EL = 8, CT_K = CT_NT * CT_EL;   // k per work item
+constexpr int CT_NT = 128;  // threads per CTA = rows of the MMA tile
 constexpr int CT_A_BYTES = 128 * 128, CT_B_BYTES = 64 * 128;  // SW128 tiles (A: 2 of 4 slices used)
 constexpr int CT_SMEM = 1024 + CT_A_BYTES + CT_B_BYTES + 64;
 // 128 registers x 128 threads cap residency at 4 CTAs per SM = 4 x 128 TMEM columns; the small shared
 // footprint lets a conversion CTA sit beside a pair-GEMM CTA whose ring leaves room (RMX_I8_STAGES)
 constexpr int CT_SMEM_REQ = (1024 + CT_A_BYTES + CT_B_BYTES + 64 + 127) / 128 * 128;
-constexpr int CT_TMEM_COLS = 128;       // 2 slices x N = 64
 static_assert(CT_SMEM <= CT_SMEM_REQ, "conversion tiles exceed the requested shared memory");
 constexpr uint32_t CT_IDESC = (2u << 4) | (static_cast<uint32_t>(64 >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 
@@ -329,10 +328,14 @@ __device__ __forceinline__ uint32_t ct_weight(int l, int b) {
   return mc.boff;
 }
 
-__global__ void __launch_bounds__(CT_NT, 4)
+// CT_EL elements (consecutive k) per thread: 8 -> 2 K-slices, 128 TMEM columns, <= 128 registers (4 CTAs
+// per SM); 4 -> 1 K-slice, 64 TMEM columns, <= 64 registers (8 CTAs per SM)
+template <int CT_EL>
+__global__ void __launch_bounds__(CT_NT, 32 / CT_EL)
     oz_convert_tc_kernel(const double *__restrict__ w, int64_t ldw, int nch, int nlev, int ne,
                          const double *__restrict__ dbuf, const float *__restrict__ xmax, int bits, int64_t ldv,
                          int8_t *__restrict__ out, int32_t *__restrict__ shift, int items_per_cta) {
+  constexpr int CT_K = CT_NT * CT_EL, CT_TMEM_COLS = 16 * CT_EL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *As = smem, *Bs = smem + CT_A_BYTES;
@@ -472,7 +475,12 @@ __global__ void __launch_bounds__(CT_NT, 4)
       if (k0 < nlev) {
         int8_t *o = out + static_cast<int64_t>(e) * L * plane + static_cast<int64_t>(i) * ldv + k0;
 #pragma unroll
-        for (int l = 0; l < L; ++l) *reinterpret_cast<uint2 *>(o + l * plane) = make_uint2(pk[l][0], pk[l][1]);
+        for (int l = 0; l < L; ++l) {
+          if (CT_EL == 8)
+            *reinterpret_cast<uint2 *>(o + l * plane) = make_uint2(pk[l][0], pk[l][CT_EL / 4 - 1]);
+          else
+            *reinterpret_cast<uint32_t *>(o + l * plane) = pk[l][0];
+        }
       }
 #pragma unroll
       for (int q = 0; q < CT_EL; ++q) dcur[q] = dnext[q];
@@ -975,11 +983,14 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
   if (ce == cudaSuccess) ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel<6>), i8::gemm2_smem(6));
   if (ce == cudaSuccess) ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_gemm2_kernel<5>), i8::gemm2_smem(5));
   if (ce != cudaSuccess) return ce;
-  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_convert_tc_kernel), i8::CT_SMEM_REQ);
+  ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_convert_tc_kernel<8>), i8::CT_SMEM_REQ);
+  if (ce == cudaSuccess) ce = ensure_smem_attr(reinterpret_cast<const void *>(i8::oz_convert_tc_kernel<4>), i8::CT_SMEM_REQ);
   if (ce != cudaSuccess) return ce;
   // X residues: byte-weight sums on the tensor cores (oz_convert_tc_kernel) unless RMX_I8_CONV_ALU is
   // set (A/B switch; read per call so that a test can compare both in one process)
   const bool conv_alu = getenv("RMX_I8_CONV_ALU") != nullptr;
+  const char *el_env = getenv("RMX_I8_CONV_EL");  // elements per thread of the tensor-core conversion (A/B)
+  const int conv_el = (el_env && atoi(el_env) == 4) ? 4 : 8;
   const int64_t ldv = rint8_ldv(nlev), ldr = rint8_ldr(nch);
   uint8_t *wsp = static_cast<uint8_t *>(ws);
   auto carve = [&](size_t bytes) {
@@ -1082,11 +1093,18 @@ cudaError_t launch_rform_int8(const double *w, int64_t ldw, const double *Ek, in
                                     static_cast<int>(std::min<int64_t>(8, n - q)), dbuf[b] + q * nlev,
                                     xmax[b] + q * nch);
     if (!x_signed && !conv_alu) {
-      const int64_t nitems = nch * ((nlev + i8::CT_K - 1) / i8::CT_K);
-      const int ipc = 4;  // work items (row, 1024 k) per CTA (16: 8.4 waves, slower)
-      i8::oz_convert_tc_kernel<<<static_cast<unsigned>((nitems + ipc - 1) / ipc), i8::CT_NT, i8::CT_SMEM_REQ, cs>>>(
-          w, ldw, static_cast<int>(nch), static_cast<int>(nlev), static_cast<int>(n), dbuf[b], xmax[b], i8::BX,
-          ldv, V[b], sx[b], ipc);
+      const int el = conv_el;
+      const int64_t nitems = nch * ((nlev + i8::CT_NT * el - 1) / (i8::CT_NT * el));
+      const int ipc = 4;  // work items (row, 128 x CT_EL k) per CTA (16 with CT_EL = 8: 8.4 waves, slower)
+      const unsigned gconv = static_cast<unsigned>((nitems + ipc - 1) / ipc);
+      if (el == 8)
+        i8::oz_convert_tc_kernel<8><<<gconv, i8::CT_NT, i8::CT_SMEM_REQ, cs>>>(
+            w, ldw, static_cast<int>(nch), static_cast<int>(nlev), static_cast<int>(n), dbuf[b], xmax[b], i8::BX,
+            ldv, V[b], sx[b], ipc);
+      else
+        i8::oz_convert_tc_kernel<4><<<gconv, i8::CT_NT, i8::CT_SMEM_REQ, cs>>>(
+            w, ldw, static_cast<int>(nch), static_cast<int>(nlev), static_cast<int>(n), dbuf[b], xmax[b], i8::BX,
+            ldv, V[b], sx[b], ipc);
     } else if (x_signed)
       i8::oz_convert_kernel<true><<<g, 256, 0, cs>>>(w, ldw, static_cast<int>(nch), static_cast<int>(nlev),
                                                          static_cast<int>(n), dbuf[b], xmax[b], rowmax, i8::BX, ldv,

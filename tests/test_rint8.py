@@ -211,15 +211,22 @@ def test_int8_tc_conversion_bitwise(ctx, nch, nlev, seed, monkeypatch):
     import torch
     c = syn.brute_force_case(nch, nlev, seed, ne=9, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
     monkeypatch.delenv("RMX_I8_CONV_ALU", raising=False)
+    monkeypatch.delenv("RMX_I8_CONV_EL", raising=False)
     R_tc, st1 = ctx.build_R(c.w, c.Ek, c.a, c.E)
     torch.cuda.synchronize()
     R_tc = R_tc.cpu().numpy()
+    monkeypatch.setenv("RMX_I8_CONV_EL", "4")  # 4 elements per thread, one K-slice per MMA
+    R_tc4, st3 = ctx.build_R(c.w, c.Ek, c.a, c.E)
+    torch.cuda.synchronize()
+    R_tc4 = R_tc4.cpu().numpy()
+    monkeypatch.delenv("RMX_I8_CONV_EL")
     monkeypatch.setenv("RMX_I8_CONV_ALU", "1")
     R_alu, st2 = ctx.build_R(c.w, c.Ek, c.a, c.E)
     torch.cuda.synchronize()
     R_alu = R_alu.cpu().numpy()
-    assert np.all(st1.cpu().numpy() == 0) and np.all(st2.cpu().numpy() == 0)
+    assert all(np.all(x.cpu().numpy() == 0) for x in (st1, st2, st3))
     assert np.array_equal(R_tc, R_alu)
+    assert np.array_equal(R_tc4, R_alu)
     for p in (0, c.ne // 2, c.ne - 1):
         ref, _ = oracle.R(c.w, c.Ek, c.a, c.E[p])
         assert nrel(R_tc[p], ref) < 1e-12
