@@ -44,6 +44,17 @@ def build_phases(verbose: bool = False, suffix: str = "", defines=()) -> str:
     return out
 
 
+def build_variant(suffix: str, defines=(), verbose: bool = False) -> str:
+    """A/B variant of the product library (librmx_<suffix>.so with extra -D flags), selected at run
+    time with RMX_LIB=... (e.g. RMX_NO_TILE_PAIRS: the row-major tile order everywhere)."""
+    out = os.path.join(PKG, f"librmx_{suffix}.so")
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd, cwd=CSRC)
+    return out
+
+
 def build_checked(force: bool = False, verbose: bool = False) -> str:
     """Bounds-checked variant (librmx_checked.so, -DRMX_CHECKS): device-side index / extent checks
     that trap (rmx_common.cuh RMX_CHECK) - the stand-in for compute-sanitizer, which is closed on
