@@ -230,3 +230,21 @@ def test_int8_tc_conversion_bitwise(ctx, nch, nlev, seed, monkeypatch):
     for p in (0, c.ne // 2, c.ne - 1):
         ref, _ = oracle.R(c.w, c.Ek, c.a, c.E[p])
         assert nrel(R_tc[p], ref) < 1e-12
+
+
+@pytest.mark.parametrize("stages", ["6", "5"])
+def test_int8_ring_depth_bitwise(ctx, stages, monkeypatch):
+    """The pair GEMM's ring depth (RMX_I8_STAGES: 7 by default, 6 / 5 leave shared memory for a
+    conversion CTA beside it - DESIGN.md §9) changes only the pipelining, never the exact int32
+    products: R bitwise equal to the default ring's, nch > 256 so the CTA-pair kernel runs (ragged
+    last column block, several 128-byte K boxes)."""
+    import torch
+    c = syn.brute_force_case(529, 1300, 21, ne=5, lo=0.5, hi=9.0, a=12.0, eps_hi=4.0)
+    monkeypatch.delenv("RMX_I8_STAGES", raising=False)
+    R7, _ = ctx.build_R(c.w, c.Ek, c.a, c.E)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("RMX_I8_STAGES", stages)
+    Rs, st = ctx.build_R(c.w, c.Ek, c.a, c.E)
+    torch.cuda.synchronize()
+    assert np.all(st.cpu().numpy() == 0)
+    assert np.array_equal(R7.cpu().numpy(), Rs.cpu().numpy())
