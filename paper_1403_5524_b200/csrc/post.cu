@@ -136,10 +136,16 @@ struct MaxwT {
 // factor is shared by all pairs (one exp per (i, T) per CTA, staged in shared memory), the second is
 // one exp per (pair, T, chunk). Where the second factor could overflow (threshold more than 600 kT
 // above the chunk start) the pair falls back to one exp per term.
-__global__ void __launch_bounds__(MAXW_PAIRS) maxwell_partial_kernel(
+// NTT: temperatures of the compiled bucket (nT <= NTT, rows t >= nT of the table are zero, so the
+// unrolled accumulation carries no per-temperature predicate; buckets 8 / 16 / 32 keep the
+// accumulators in registers - one kernel for RMX_MAX_TEMPS = 32 spent half its FMAs on padding rows
+// and its instruction fetch on predicated code). Points at or below threshold get the weight 0
+// instead of a branch (E ascending: they form a prefix of the chunk).
+template <int NTT>
+__global__ void __launch_bounds__(MAXW_PAIRS, NTT <= 16 ? 4 : 2) maxwell_partial_kernel(
     const double *__restrict__ omega, int64_t ne, int64_t npair, const double *__restrict__ E,
     const double *__restrict__ Eth, const MaxwT T, double *__restrict__ part) {
-  __shared__ double sE[RMX_MAX_TEMPS][MAXW_CHUNK];
+  __shared__ __align__(16) double sE[MAXW_CHUNK][NTT];  // [point][T]: a point's factors read as double2
   __shared__ double sx[MAXW_CHUNK + 2];  // E_{c0-1} .. E_{c1}
   const int64_t p = static_cast<int64_t>(blockIdx.x) * MAXW_PAIRS + threadIdx.x;
   const int64_t c = blockIdx.y;
@@ -151,58 +157,66 @@ __global__ void __launch_bounds__(MAXW_PAIRS) maxwell_partial_kernel(
   }
   __syncthreads();
   const double Ec0 = sx[1];
-  for (int q = threadIdx.x; q < T.nT * MAXW_CHUNK; q += MAXW_PAIRS) {
-    const int t = q / MAXW_CHUNK, ii = q % MAXW_CHUNK;
-    sE[t][ii] = (ii < n) ? exp(-(sx[ii + 1] - Ec0) / T.kT[t]) : 0.0;
+  for (int q = threadIdx.x; q < NTT * MAXW_CHUNK; q += MAXW_PAIRS) {
+    const int ii = q / NTT, t = q % NTT;
+    sE[ii][t] = (ii < n && t < T.nT) ? exp(-(sx[ii + 1] - Ec0) / T.kT[t]) : 0.0;
   }
   __syncthreads();
   if (p >= npair) return;
   const double eth = Eth[p];
-  double acc[RMX_MAX_TEMPS];
+  double acc[NTT];
 #pragma unroll
-  for (int t = 0; t < RMX_MAX_TEMPS; ++t) acc[t] = 0.0;
+  for (int t = 0; t < NTT; ++t) acc[t] = 0.0;
   bool direct = false;
+  for (int t = 0; t < T.nT; ++t) direct |= (eth - Ec0) / T.kT[t] > 600.0;
+  auto weight = [&](int ii) {  // trapezoid weight of point c0 + ii (0 if not above threshold)
+    const int64_t i = c0 + ii;
+    const double Ei = sx[ii + 1];
+    if (ii >= n || !(Ei > eth)) return 0.0;
+    // half the interval to the right (if any) plus half the interval to the left when the left
+    // neighbour is also above threshold
+    const double right = (i + 1 < ne) ? 0.5 * (sx[ii + 2] - Ei) : 0.0;
+    const double left = (i > 0 && sx[ii] > eth) ? 0.5 * (Ei - sx[ii]) : 0.0;
+    return right + left;
+  };
+  if (!direct) {
+    // Omega loads issued in groups of PF (independent of the accumulation; latency-bound otherwise)
+    constexpr int PF = NTT <= 8 ? 8 : 4;
+    for (int g0 = 0; g0 < n; g0 += PF) {
+      double ob[PF];
 #pragma unroll
-  for (int t = 0; t < RMX_MAX_TEMPS; ++t) direct |= (t < T.nT) && (eth - Ec0) / T.kT[t] > 600.0;
-  // Omega loads issued in groups of 8 (independent of the accumulation; the loop is latency-bound
-  // otherwise)
-  constexpr int PF = 8;
-  for (int g0 = 0; g0 < n; g0 += PF) {
-    double ob[PF];
+      for (int q = 0; q < PF; ++q) ob[q] = (g0 + q < n) ? omega[(c0 + g0 + q) * npair + p] : 0.0;
 #pragma unroll
-    for (int q = 0; q < PF; ++q) ob[q] = (g0 + q < n) ? omega[(c0 + g0 + q) * npair + p] : 0.0;
+      for (int q = 0; q < PF; ++q) {
+        const double wq = weight(g0 + q);
+        const double om = wq != 0.0 ? wq * ob[q] : 0.0;  // Omega below threshold never read into the sum
+        const double2 *ep = reinterpret_cast<const double2 *>(sE[g0 + q]);
 #pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int ii = g0 + q;
-      if (ii >= n) break;
-      const int64_t i = c0 + ii;
-      const double Ei = sx[ii + 1];
-      if (!(Ei > eth)) continue;  // point not above threshold (E ascending: a prefix of the chunk)
-      // trapezoid weight: half the interval to the right (if any) plus half the interval to the
-      // left when the left neighbour is also above threshold
-      const double right = (i + 1 < ne) ? 0.5 * (sx[ii + 2] - Ei) : 0.0;
-      const double left = (i > 0 && sx[ii] > eth) ? 0.5 * (Ei - sx[ii]) : 0.0;
-      const double om = (right + left) * ob[q];
-      if (!direct) {
-#pragma unroll
-        for (int t = 0; t < RMX_MAX_TEMPS; ++t)
-          if (t < T.nT) acc[t] = fma(om, sE[t][ii], acc[t]);
-      } else {
-#pragma unroll
-        for (int t = 0; t < RMX_MAX_TEMPS; ++t)
-          if (t < T.nT) acc[t] = fma(om, exp(-(Ei - eth) / T.kT[t]), acc[t]);
+        for (int t2 = 0; t2 < NTT / 2; ++t2) {
+          const double2 f = ep[t2];
+          acc[2 * t2] = fma(om, f.x, acc[2 * t2]);
+          acc[2 * t2 + 1] = fma(om, f.y, acc[2 * t2 + 1]);
+        }
       }
+    }
+  } else {  // threshold > 600 kT above the chunk start for some T: one exp per term (rare)
+#pragma unroll 1
+    for (int ii = 0; ii < n; ++ii) {
+      const double om = weight(ii);
+      if (om == 0.0) continue;
+      const double ov = om * omega[(c0 + ii) * npair + p], Ei = sx[ii + 1];
+#pragma unroll
+      for (int t = 0; t < NTT; ++t)
+        if (t < T.nT) acc[t] = fma(ov, exp(-(Ei - eth) / T.kT[t]), acc[t]);
     }
   }
 #pragma unroll
-  for (int t = 0; t < RMX_MAX_TEMPS; ++t) {
+  for (int t = 0; t < NTT; ++t) {
     if (t >= T.nT) break;
     const double f = direct ? 1.0 : exp(-(Ec0 - eth) / T.kT[t]);
     part[(c * npair + p) * T.nT + t] = acc[t] * f / T.kT[t];
   }
 }
-
-// One warp per output (pair, T): lane l adds chunks l, l + 32, ... in order, then a fixed xor tree.
 __global__ void maxwell_reduce_kernel(const double *__restrict__ part, int64_t nchunk, int64_t npair,
                                       int nT, double *__restrict__ ups) {
   const int64_t q = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
@@ -253,7 +267,12 @@ cudaError_t launch_maxwell(const double *omega, int64_t ne, int64_t npair, const
   T.nT = nT;
   const int64_t nchunk = maxwell_chunks(ne);
   dim3 grid(static_cast<unsigned>((npair + MAXW_PAIRS - 1) / MAXW_PAIRS), static_cast<unsigned>(nchunk));
-  maxwell_partial_kernel<<<grid, MAXW_PAIRS, 0, st>>>(omega, ne, npair, E, Eth, T, part);
+  if (nT <= 8)
+    maxwell_partial_kernel<8><<<grid, MAXW_PAIRS, 0, st>>>(omega, ne, npair, E, Eth, T, part);
+  else if (nT <= 16)
+    maxwell_partial_kernel<16><<<grid, MAXW_PAIRS, 0, st>>>(omega, ne, npair, E, Eth, T, part);
+  else
+    maxwell_partial_kernel<32><<<grid, MAXW_PAIRS, 0, st>>>(omega, ne, npair, E, Eth, T, part);
   const int64_t nq = npair * nT;
   maxwell_reduce_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(part, nchunk, npair,
                                                                                      nT, ups);

@@ -122,14 +122,21 @@ def test_gpu_convolve(ctx, ne, dE, fwhm):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nT", [7, 20])
-def test_gpu_maxwell(ctx, nT):
+@pytest.mark.parametrize("nT,nan_below", [(1, False), (7, False), (16, False), (16, True), (20, False),
+                                          (32, False)])
+def test_gpu_maxwell(ctx, nT, nan_below):
+    """Maxwell average against the oracle for every temperature bucket of the kernel (8 / 16 / 32);
+    nan_below: Omega holds NaN at the points not above a pair's threshold, which reading U1 never
+    integrates (the oracle starts at the first point above threshold) - the GPU must not read them
+    into the sum either."""
     import torch
     rng = np.random.default_rng(4)
     ne, npair = 5000, 700
     E = 0.5 + np.arange(ne) * (59.5 / (ne - 1))
     Eth = np.sort(rng.uniform(0.0, 50.0, npair))
     om = rng.uniform(0.0, 3.0, (ne, npair)) * (E[:, None] > Eth[None, :])
+    if nan_below:
+        om[~(E[:, None] > Eth[None, :])] = np.nan
     kT = list(np.geomspace(0.03, 60.0, nT))
     ups = ctx.maxwell_average(om, E, Eth, kT).cpu().numpy()
     torch.cuda.synchronize()
